@@ -1,0 +1,400 @@
+"""Benchmark: seconds per video of the PAB denoising loop on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+A bench "step" is one whole video: the 30-step (config-dependent) PAB
+denoising loop of BASELINE.json's headline config C3 (Open-Sora 1.2-shaped
+STDiT, 2s 480p: L28 D1152 H16 dh72, T16 S1560 M300, cross attention in the
+temporal block, CFG batch 2, preset opensora-pab246), random-init weights
+and synthetic seeded inputs.  ``value`` = device time per video with the
+latent resident in HBM; ``e2e`` = the same through the public serving call
+(pinned host x_T -> H2D -> denoise -> D2H of the final latent).
+
+Under torchrun (N > 1) the video is sharded with broadcast sequence
+parallelism (frames across ranks, NCCL all-to-all around temporal attention,
+skipped on temporal-broadcast steps): strong scaling of one video.
+
+--impl reference times the reference algorithm's CPU implementation (the
+numpy oracle, all host threads) on a bounded sample of the same workload and
+extrapolates to s/video by FLOP count.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # SURVEY.md section 8 config key
+    "C1": dict(layers=4, hidden=144, heads=2, frames=8, spatial_tokens=1024, text_tokens=16, cross=False, steps=10,
+               preset="latte-pab235", batch=1),
+    "C2": dict(layers=28, hidden=1152, heads=16, frames=16, spatial_tokens=1024, text_tokens=120, cross=False,
+               steps=50, preset="latte-pab235", batch=2),
+    "C3": dict(layers=28, hidden=1152, heads=16, frames=16, spatial_tokens=1560, text_tokens=300, cross=True,
+               steps=30, preset="opensora-pab246", batch=2),
+    "C4": dict(layers=28, hidden=1152, heads=16, frames=16, spatial_tokens=1024, text_tokens=300, cross=False,
+               steps=150, preset="opensoraplan-pab246", batch=2),
+    "C5": dict(layers=28, hidden=1152, heads=16, frames=32, spatial_tokens=3600, text_tokens=300, cross=True,
+               steps=30, preset="opensora-pab246", batch=2),
+}
+METRIC = "s/video denoising latency (PAB, opensora-pab246)"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def model_config(c):
+    from paper_2408_12588_b200.model import ModelConfig
+
+    return ModelConfig(layers=c["layers"], hidden=c["hidden"], heads=c["heads"], frames=c["frames"],
+                       spatial_tokens=c["spatial_tokens"], text_tokens=c["text_tokens"],
+                       cross_in_temporal=c["cross"])
+
+
+def video_flops(cfg, table, batch):
+    """Algorithmic flops of one video under a decision table (2 flop/MAC, all
+    GEMMs + attention contractions of computed sites; reference profiler
+    flop model, profiler.py:176-226, without elementwise constants)."""
+    import numpy as np
+
+    D, R, T, S, M, H = cfg.hidden, cfg.mlp_hidden, cfg.frames, cfg.spatial_tokens, cfg.text_tokens, cfg.heads
+    rows = batch * T * S
+    site = {
+        "spatial": 2 * rows * D * 3 * D + 4 * batch * T * S * S * D + 2 * rows * D * D,
+        "temporal": 2 * rows * D * 3 * D + 4 * batch * S * T * T * D + 2 * rows * D * D,
+        "cross": 2 * rows * D * D + 4 * rows * M * D + 2 * rows * D * D,
+        "mlp": 2 * 2 * rows * D * R,
+    }
+    mult = {"spatial": 1, "temporal": 1, "cross": 1 + int(cfg.cross_in_temporal), "mlp": 2}
+    comp = table.compute_mask()
+    total = 0
+    for k, name in enumerate(("spatial", "temporal", "cross", "mlp")):
+        total += int(np.count_nonzero(comp[:, :, k])) * site[name] * mult[name]
+    return total, site
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/pab_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(c, max_seconds=30.0):
+    """Time the numpy oracle (reference algorithm, all host threads via BLAS) on
+    one all-compute layer-step of the workload at batch 1 and extrapolate to
+    s/video with the video's FLOP count."""
+    import numpy as np
+
+    from oracle import pab_oracle as orc
+    from paper_2408_12588_b200.diffusion import make_schedule
+    from paper_2408_12588_b200.policies import build_schedule, resolve_preset
+
+    cfg = model_config(c)
+    ocfg = orc.Cfg(1, c["hidden"], c["heads"], c["frames"], c["spatial_tokens"], c["text_tokens"],
+                   cross_in_temporal=c["cross"])
+    w = orc.init_weights(ocfg, seed=11)
+    table = np.zeros((1, 1, 4), dtype=np.int32)
+    x = orc.latent0(ocfg, 11, 1)
+    text = orc.text_embedding(w, (np.arange(c["text_tokens"]) % 256)[None])
+    reps, spent = 0, 0.0
+    while reps < 1 or (spent < max_seconds / 3 and reps < 3):
+        t0 = time.perf_counter()
+        orc.forward(ocfg, w, x, 500.0, text, table, 0, {})
+        spent += time.perf_counter() - t0
+        reps += 1
+    per_layer_step = spent / reps
+    sched = make_schedule(c["steps"])
+    pol, _ = resolve_preset(c["preset"], c["layers"])
+    tab = build_schedule(pol, sched, c["layers"])
+    flops_video, _ = video_flops(cfg, tab, c["batch"])
+    sample_table = type(tab)(np.zeros((1, 1, 4), dtype=np.int32))
+    ocfg_model = model_config(dict(c, layers=1))
+    flops_sample, _ = video_flops(ocfg_model, sample_table, 1)
+    s_per_video = per_layer_step * flops_video / flops_sample
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    return {
+        "value": s_per_video, "unit": "s/video", "cores": cores, "kind": "port",
+        "sample": (f"numpy oracle (reference algorithm, BLAS matmul) on 1 layer x 1 step x batch 1, all sites "
+                   f"computed, at {c['spatial_tokens']} tokens x {c['frames']} frames x D{c['hidden']}: "
+                   f"{per_layer_step:.2f} s/layer-step over {reps} reps, extrapolated x{flops_video / flops_sample:.0f} "
+                   f"by algorithmic FLOPs to the full PAB video"),
+    }
+
+
+def run_reference(args, c):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    times = []
+    base = None
+    for _ in range(args.warmup + args.steps):
+        base = cpu_baseline(c, max_seconds=20.0)
+        times.append(base["value"])
+    vals = times[args.warmup:]
+    v = statistics.median(vals)
+    base["value"] = v
+    line = {
+        "metric": METRIC, "value": v, "unit": "s/video", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": v * 1000.0, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded splitmix64 weights and x_T)",
+        "config": {"workload": args.config, **{k: c[k] for k in ("layers", "hidden", "heads", "frames",
+                                                                     "spatial_tokens", "text_tokens", "steps",
+                                                                     "batch", "preset")}},
+        "impl": "reference", "cpu_baseline": base,
+        "e2e": {"value": v, "unit": "s/video", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-none", action="store_true", help="skip the no-PAB comparison run")
+    args = ap.parse_args()
+    c = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, c)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2408_12588_b200 import kernels
+    from paper_2408_12588_b200.diffusion import Denoiser, initial_latent, make_schedule
+    from paper_2408_12588_b200.model import init_model
+    from paper_2408_12588_b200.policies import NonePolicy, build_schedule, resolve_preset
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = model_config(c)
+    params = init_model(cfg, seed=11)
+    sched = make_schedule(c["steps"])
+    pol, _ = resolve_preset(c["preset"], cfg.layers)
+    table = build_schedule(pol, sched, cfg.layers)
+    ids = np.arange(cfg.text_tokens) % 256
+    guidance = c["batch"] == 2
+
+    if world > 1:
+        from paper_2408_12588_b200.parallel import ShardedDenoiser
+
+        den = ShardedDenoiser(params, sched, table, ids, guidance=guidance, guidance_scale=4.0, rank=rank,
+                              world=world)
+    else:
+        den = Denoiser(params, sched, table, ids, guidance=guidance, guidance_scale=4.0)
+    x_host = torch.from_numpy(initial_latent(params, 11, c["batch"])).pin_memory()
+    x_dev = den.shard_input(x_host.cuda()) if world > 1 else x_host.cuda()
+    z = torch.empty_like(x_dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def one_video():
+        z.copy_(x_dev)
+        den.run(z)
+
+    for _ in range(args.warmup):
+        one_video()
+    barrier()
+    launches0 = den.ctx.launches.own_kernels()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            one_video()
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    launches = (den.ctx.launches.own_kernels() - launches0) // args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # e2e through the public serving call: pinned host x_T -> H2D -> denoise -> D2H latent
+    out_host = torch.empty_like(x_host).pin_memory()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        den(x_host, out=out_host)
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    io_bytes = x_host.numel() * x_host.element_size()
+
+    # no-PAB reference point (same engine, every site computed)
+    none_ms = None
+    if not args.no_none:
+        table_none = build_schedule(NonePolicy(), sched, cfg.layers)
+        if world > 1:
+            den_none = ShardedDenoiser(params, sched, table_none, ids, guidance=guidance, guidance_scale=4.0,
+                                       rank=rank, world=world)
+        else:
+            den_none = Denoiser(params, sched, table_none, ids, guidance=guidance, guidance_scale=4.0)
+        z.copy_(x_dev)
+        den_none.run(z)
+        barrier()
+        n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n0.record(stream)
+        reps = max(1, args.steps // 2)
+        for _ in range(reps):
+            z.copy_(x_dev)
+            den_none.run(z)
+        n1.record(stream)
+        barrier()
+        none_ms = n0.elapsed_time(n1) / reps
+        if world > 1:
+            t = torch.tensor([none_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            none_ms = float(t.item())
+        del den_none
+
+    # roofline of the dominant kernel (spatial attention), timed live on the launching stream
+    peaks, peak_src = load_peaks()
+    ctx = den.ctx
+    kern = {}
+
+    def time_launch(fn, reps=10):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps / 1000.0
+
+    B, T, S, D, M = ctx.B, ctx.T, ctx.S, ctx.D, ctx.M
+    flop_sp = 4.0 * B * T * S * S * D
+    t_sp = time_launch(lambda: kernels.attention(ctx.args_spatial))
+    flop_tm = 4.0 * B * S * T * T * D
+    t_tm = time_launch(lambda: kernels.attention(ctx.args_temporal))
+    flop_cr = 4.0 * B * T * S * M * D
+    t_cr = time_launch(lambda: kernels.attention(ctx.args_cross[0][0]))
+    rows = ctx.rows
+    xbuf = torch.zeros(rows, D, device="cuda")
+    pend = [torch.zeros(rows, D, device="cuda", dtype=torch.bfloat16)]
+    mod = torch.zeros(2 * D, device="cuda")
+    t_mn = time_launch(lambda: kernels.residual_modnorm(xbuf, xbuf, pend, h_out=ctx.h, mod=mod, mode=1))
+    bytes_mn = rows * D * (4 + 2 + 4 + 2)
+    kern = {
+        "spatial_attn": {"ms": t_sp * 1e3, "tflops": flop_sp / t_sp / 1e12,
+                         "frac_bf16_peak": flop_sp / t_sp / 1e12 / peaks["bf16_tflops"]},
+        "temporal_attn": {"ms": t_tm * 1e3, "gbs": 8.0 * B * T * S * D / t_tm / 1e9,
+                          "frac_hbm": 8.0 * B * T * S * D / t_tm / 1e9 / peaks["hbm_gbs"]},
+        "cross_attn": {"ms": t_cr * 1e3, "tflops": flop_cr / t_cr / 1e12,
+                       "gbs": (4.0 * B * T * S * D + 4.0 * B * M * D) / t_cr / 1e9},
+        "broadcast_epilogue_modnorm": {"ms": t_mn * 1e3, "gbs": bytes_mn / t_mn / 1e9,
+                                       "frac_hbm": bytes_mn / t_mn / 1e9 / peaks["hbm_gbs"]},
+    }
+    achieved = flop_sp / t_sp / 1e12
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / peaks["bf16_tflops"], "traffic": None, "kernel": "attn_tc_kernel (spatial)",
+                "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
+                "algorithmic_flops_per_launch": flop_sp}
+    flops_pab, _ = video_flops(cfg, table, c["batch"])
+
+    if rank == 0:
+        base = None if args.no_cpu_baseline else cpu_baseline(c)
+        line = {
+            "metric": METRIC, "value": ms / 1000.0, "unit": "s/video", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded splitmix64 weights and x_T)",
+            "config": {"workload": args.config, "layers": cfg.layers, "hidden": cfg.hidden, "heads": cfg.heads,
+                       "frames": cfg.frames, "spatial_tokens": cfg.spatial_tokens, "text_tokens": cfg.text_tokens,
+                       "denoise_steps": c["steps"], "batch": c["batch"], "preset": c["preset"],
+                       "parallelism": f"broadcast_sp{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (fp32 latent 230 MB > 126 MB L2)",
+                       "none_s_per_video": None if none_ms is None else none_ms / 1000.0,
+                       "pab_speedup_vs_none": None if none_ms is None else none_ms / ms,
+                       "video_tflop_pab": flops_pab / 1e12, "achieved_tflops_video": flops_pab / (ms / 1e3) / 1e12},
+            "e2e": {"value": e2e_ms / 1000.0, "unit": "s/video", "h2d_bytes_per_step": io_bytes,
+                    "d2h_bytes_per_step": io_bytes},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "kernels": kern,
+            "clocks": clk.summary(),
+            "cpu_baseline": base,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

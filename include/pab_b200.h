@@ -1,0 +1,122 @@
+/*
+ * pab_b200.h -- C ABI of the B200-native Pyramid Attention Broadcast hot path.
+ *
+ * Every entry point takes plain device pointers, element counts/strides and a
+ * cudaStream_t passed as void*; the library never allocates or frees device
+ * memory (the caller -- PyTorch in this repo -- owns every buffer) and never
+ * throws across the ABI.  Calls are asynchronous on `stream` and capturable
+ * into CUDA graphs.  Return value: 0 on success, else a PAB_ERR_* code that
+ * the Python wrapper maps back onto the reference's EngineError kinds
+ * (reference pkg/src/pab_engine/errors.py:4-40).
+ *
+ * The reference (pab-engine) is pure Python/numpy; its "operator API" is the
+ * set of module functions the denoising loop calls.  Each entry point below
+ * names the reference function(s) it replaces.
+ */
+#ifndef PAB_B200_H
+#define PAB_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PAB_OK 0
+#define PAB_ERR_SHAPE 1       /* reference ShapeError   "shape-mismatch" */
+#define PAB_ERR_INVALID 2     /* reference ValidationError "invalid-config" */
+#define PAB_ERR_POLICY 3      /* reference PolicyError  "policy-error" */
+#define PAB_ERR_CUDA 4        /* CUDA / driver failure (DeviceError) */
+#define PAB_ERR_UNSUPPORTED 5 /* shape outside what a kernel supports */
+
+#define PAB_MAX_PENDING 8     /* pending residual terms per launch */
+
+/* Library metadata. */
+const char* pab_version(void);
+const char* pab_status_string(int status);
+/* Last CUDA error string recorded by a failing call (thread-local). */
+const char* pab_last_error(void);
+
+/*
+ * Broadcast epilogue + modulated-norm prologue (kernels K4+K5).
+ * Replaces: model.run_site's `x + o` residual add for computed AND reused
+ * sites (pkg/src/pab_engine/model.py:469-503), `_modulated_norm`
+ * (model.py:317-324) and `layer_norm` (numerics.py:115-130).
+ *
+ *   x_out[r, :] = x_in[r, :] + pending[0][r, :] + ... + pending[n-1][r, :]   (fp32, in order)
+ *   mode 0: no h output
+ *   mode 1: h = bf16( (LN(x_out) * gamma + beta) * (1 + mod[D:2D]) + mod[0:D] )
+ *   mode 2: h = bf16( x_out )   (cross-attention query input, no norm)
+ * x_in may equal x_out.  pending[i] are bf16 (rows, D) row-major.
+ * gamma/beta may be NULL (identity affine).  n_pending <= PAB_MAX_PENDING.
+ */
+int pab_residual_modnorm(const float* x_in, float* x_out,
+                         const void* const* pending, int n_pending,
+                         const float* gamma, const float* beta,
+                         const float* mod, void* h_out,
+                         int64_t rows, int D, float eps, int mode, void* stream);
+
+/*
+ * Fused end-of-step residual drain + classifier-free guidance + DDIM (K8).
+ * Replaces: the eps combine and ddim_update of diffusion.sample
+ * (pkg/src/pab_engine/diffusion.py:183-189, 100-103).
+ *   eps_b = r[b] + pending terms (fp32, in order)
+ *   guidance: eps_hat = eps_1 + g * (eps_0 - eps_1), applied to every batch row
+ *   z[b] = sqrt(a_next) * ((z[b] - sqrt(1-a_cur) * eps_hat) / sqrt(a_cur)) + sqrt(1-a_next) * eps_hat
+ * All scalars are rounded to fp32 first and every op is a single fp32
+ * rounding, as numpy does with python-float scalars on float32 arrays.
+ */
+int pab_ddim_cfg(float* z, const float* r, const void* const* pending, int n_pending,
+                 int batch, int64_t n_per_batch, int guidance, double guidance_scale,
+                 double a_cur, double a_next, void* stream);
+
+/* tanh-approximation GELU on bf16 (numerics.py:154-158), in may equal out. */
+int pab_gelu_bf16(const void* in, void* out, int64_t n, void* stream);
+
+/*
+ * splitmix64 parameter fill (model.init_model + numerics.RandomStream.uniform,
+ * pkg/src/pab_engine/model.py:168-222, numerics.py:161-201).
+ * Element i (i < rows*cols) takes draw (first_draw + i + 1) of the stream
+ * whose state is `state`: v = f32(lo + (mant53 * 2^-53) * (hi - lo)).
+ * It is written to dst[(i / cols) * ld + col0 + (i % cols)] as fp32
+ * (dtype 0) or bf16 (dtype 1).
+ */
+int pab_fill_uniform(void* dst, int dtype, int64_t rows, int64_t cols, int64_t ld, int64_t col0,
+                     uint64_t state, uint64_t first_draw, double lo, double hi, void* stream);
+
+/*
+ * Multi-head scaled-dot-product attention softmax(q k^T / sqrt(dh)) v (K1-K3).
+ * Replaces: scaled_dot_attention (numerics.py:133-151) as called by the
+ * spatial / temporal / cross sites (model.py:327-385).
+ *
+ * Problem (a, b, h), a < n_a, b < n_b, h < heads, attends n_q query rows to
+ * n_k key rows.  Element (a, b, h, i, d) of tensor X lives at
+ *   X + a*X_sa + b*X_sb + i*X_si + h*dh + d        (element units, bf16)
+ * so spatial, temporal (transposed) and cross layouts need no copies:
+ *   spatial : a = frame (B*T), b = -, i = token     (rows of (B,T,S,D))
+ *   temporal: a = batch, b = token, i = frame        (rows of (B,T,S,D))
+ *   cross   : a = batch, i = (frame, token) for q/o, i = text token for k/v
+ * Output o uses the same addressing with (o_sa, o_sb, o_si).
+ * impl: 0 = auto (tcgen05/TMA kernel when the shape allows), 1 = force the
+ * tcgen05 kernel (error if unsupported), 2 = force the SIMT kernel.
+ */
+typedef struct {
+    const void* q; const void* k; const void* v; void* o;
+    int64_t q_sa, q_sb, q_si;
+    int64_t k_sa, k_sb, k_si;
+    int64_t v_sa, v_sb, v_si;
+    int64_t o_sa, o_sb, o_si;
+    int32_t n_a, n_b, n_q, n_k, heads, dh;
+    float scale;
+} pab_attn_args;
+
+int pab_attention(const pab_attn_args* args, int impl, void* stream);
+
+/* Which attention implementation `impl=0` would select for these args
+ * (1 = tcgen05, 2 = SIMT).  Pure host logic, no GPU needed. */
+int pab_attention_select(const pab_attn_args* args);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PAB_B200_H */

@@ -1,0 +1,127 @@
+// Attention dispatcher + the SIMT attention kernel.
+//
+// The production path for the model's shapes is the tcgen05/TMEM/TMA kernel
+// in attn_tc.cu.  The SIMT kernel here covers the shapes TMA cannot address
+// (head dim not a multiple of 8, row strides not 16-byte aligned -- e.g. the
+// reference's tiny hypothesis configs with hidden 8) and serves as an
+// independent on-device cross-check in the GPU tests.
+//
+// reference: numerics.scaled_dot_attention (pkg/src/pab_engine/numerics.py:133-151):
+//   logits = q k^T; logits *= 1/sqrt(dh); softmax over keys (max-shifted); out = p v
+#include "common.cuh"
+#include <math.h>
+
+namespace pab {
+
+int attn_tc_launch(const pab_attn_args* a, cudaStream_t st);  // attn_tc.cu
+bool attn_tc_supported(const pab_attn_args* a);                 // attn_tc.cu
+
+namespace {
+
+constexpr int kSimtWarps = 8;   // query rows per block
+constexpr int kSimtKeys = 32;   // keys per smem tile
+constexpr int kSimtMaxDh = 128;
+
+__global__ void __launch_bounds__(kSimtWarps * 32) attn_simt_kernel(pab_attn_args a) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int h = blockIdx.y;
+    const int64_t ab = blockIdx.z;
+    const int64_t ia = ab / a.n_b, ib = ab - ia * a.n_b;
+    const int dh = a.dh;
+    const int ldk = dh + 1;  // odd word-free padding against bank conflicts (fp32 tiles)
+    __shared__ float ks[kSimtKeys * (kSimtMaxDh + 1)];
+    __shared__ float vs[kSimtKeys * (kSimtMaxDh + 1)];
+    __shared__ float qs[kSimtWarps][kSimtMaxDh];
+
+    const __nv_bfloat16* q = reinterpret_cast<const __nv_bfloat16*>(a.q) + ia * a.q_sa + ib * a.q_sb + (int64_t)h * dh;
+    const __nv_bfloat16* k = reinterpret_cast<const __nv_bfloat16*>(a.k) + ia * a.k_sa + ib * a.k_sb + (int64_t)h * dh;
+    const __nv_bfloat16* v = reinterpret_cast<const __nv_bfloat16*>(a.v) + ia * a.v_sa + ib * a.v_sb + (int64_t)h * dh;
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(a.o) + ia * a.o_sa + ib * a.o_sb + (int64_t)h * dh;
+
+    const int row = blockIdx.x * kSimtWarps + warp;
+    const bool active = row < a.n_q;
+    if (active)
+        for (int d = lane; d < dh; d += 32) qs[warp][d] = __bfloat162float(q[(int64_t)row * a.q_si + d]);
+
+    float m = -INFINITY, l = 0.f;
+    float acc[kSimtMaxDh / 32];
+#pragma unroll
+    for (int e = 0; e < kSimtMaxDh / 32; ++e) acc[e] = 0.f;
+
+    for (int j0 = 0; j0 < a.n_k; j0 += kSimtKeys) {
+        __syncthreads();
+        const int nk = min(kSimtKeys, a.n_k - j0);
+        for (int idx = threadIdx.x; idx < nk * dh; idx += blockDim.x) {
+            const int j = idx / dh, d = idx - j * dh;
+            ks[j * ldk + d] = __bfloat162float(k[(int64_t)(j0 + j) * a.k_si + d]);
+            vs[j * ldk + d] = __bfloat162float(v[(int64_t)(j0 + j) * a.v_si + d]);
+        }
+        __syncthreads();
+        if (!active) continue;
+        float s = -INFINITY;
+        if (lane < nk) {
+            float dot = 0.f;
+            for (int d = 0; d < dh; ++d) dot += qs[warp][d] * ks[lane * ldk + d];
+            s = dot * a.scale;
+        }
+        const float m_new = fmaxf(m, warp_max(s));
+        const float p = (lane < nk) ? expf(s - m_new) : 0.f;
+        const float corr = expf(m - m_new);  // m = -inf on the first tile -> 0
+        l = l * corr + warp_sum(p);
+#pragma unroll
+        for (int e = 0; e < kSimtMaxDh / 32; ++e) acc[e] *= corr;
+        for (int j = 0; j < nk; ++j) {
+            const float pj = __shfl_sync(0xffffffffu, p, j);
+#pragma unroll
+            for (int e = 0; e < kSimtMaxDh / 32; ++e) {
+                const int d = lane + 32 * e;
+                if (d < dh) acc[e] += pj * vs[j * ldk + d];
+            }
+        }
+        m = m_new;
+    }
+    if (!active) return;
+    const float inv = (a.n_k > 0) ? 1.0f / l : 0.f;
+#pragma unroll
+    for (int e = 0; e < kSimtMaxDh / 32; ++e) {
+        const int d = lane + 32 * e;
+        if (d < dh) o[(int64_t)row * a.o_si + d] = __float2bfloat16_rn(acc[e] * inv);
+    }
+}
+
+int attn_simt_launch(const pab_attn_args* a, cudaStream_t st) {
+    if (a->dh > kSimtMaxDh) return PAB_ERR_UNSUPPORTED;
+    const int64_t nab = (int64_t)a->n_a * a->n_b;
+    if (nab > 65535 || a->heads > 65535) return PAB_ERR_UNSUPPORTED;
+    dim3 grid((unsigned)((a->n_q + kSimtWarps - 1) / kSimtWarps), (unsigned)a->heads, (unsigned)nab);
+    attn_simt_kernel<<<grid, kSimtWarps * 32, 0, st>>>(*a);
+    return launch_status("attn_simt");
+}
+
+bool args_valid(const pab_attn_args* a) {
+    return a && a->q && a->k && a->v && a->o && a->n_a >= 0 && a->n_b >= 0 && a->n_q >= 0 &&
+           a->n_k >= 0 && a->heads >= 1 && a->dh >= 1;
+}
+
+}  // namespace
+}  // namespace pab
+
+using namespace pab;
+
+extern "C" int pab_attention_select(const pab_attn_args* a) {
+    if (!args_valid(a)) return 0;
+    return attn_tc_supported(a) ? 1 : 2;
+}
+
+extern "C" int pab_attention(const pab_attn_args* a, int impl, void* stream) {
+    if (!args_valid(a)) return PAB_ERR_SHAPE;
+    if (a->n_a == 0 || a->n_b == 0 || a->n_q == 0) return PAB_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (impl == 0) impl = attn_tc_supported(a) ? 1 : 2;
+    if (impl == 1) {
+        if (!attn_tc_supported(a)) return PAB_ERR_UNSUPPORTED;
+        return attn_tc_launch(a, st);
+    }
+    if (impl == 2) return attn_simt_launch(a, st);
+    return PAB_ERR_INVALID;
+}

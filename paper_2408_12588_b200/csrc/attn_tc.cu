@@ -1,0 +1,623 @@
+// tcgen05 / TMEM / TMA flash attention for sm_100a (kernels K1-K3).
+//
+// reference op: numerics.scaled_dot_attention (pkg/src/pab_engine/numerics.py:133-151)
+// as used by the spatial, temporal and cross sites (model.py:327-385).
+//
+// CTA layout (320 threads, one CTA per SM):
+//   warps 0-3  softmax group 0  -> query tile 0 (128 rows, 1 thread = 1 row = 1 TMEM lane)
+//   warps 4-7  softmax group 1  -> query tile 1
+//   warp  8    TMA producer (one elected lane)
+//   warp  9    TMEM allocator + MMA issuer (one elected lane)
+// Per KV tile j the MMA lane issues, ping-ponging the two query tiles,
+//   S_i = Q_i K_j^T  (M=128, N=128, K=dh padded to 16)  -> TMEM cols [128 i, 128 i + 128)
+//   O_i += P_i V_j   (M=128, N=64|16 blocks, K=128)      -> TMEM cols [256 + 128 i, ...)
+// while group i turns S_i into P_i (bf16, smem) with an online softmax whose
+// running max is only raised (and O rescaled in TMEM) when it grows by more
+// than 2^8, so P stays <= 256 and the O correction is rare.
+//
+// Head dim: dh is split into 64-wide K blocks staged with 128B swizzle plus
+// 16-wide blocks with 32B swizzle; the TMA box of the last block runs past dh
+// and the hardware zero-fills the padding (72 -> 64 + 16 with 8 zero columns).
+//
+// "Packed" mode (temporal attention, sequence length T <= 64): one 128-row
+// tile holds floor(128/T) independent sequences (consecutive tokens b) and the
+// softmax masks the block diagonal, so the short problems still run on
+// 128x128 tensor-core tiles; the kernel is HBM-bound there.
+#include "common.cuh"
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <math.h>
+#include <mutex>
+
+namespace pab {
+
+namespace tc {
+
+constexpr int kThreads = 320;
+constexpr int kRows = 128;       // query rows per tile == TMEM lanes
+constexpr int kKv = 128;         // keys per KV tile
+constexpr int kPBytes = kRows * kKv * 2;
+constexpr uint32_t kTmemCols = 512;
+
+struct Params {
+    int n_q, n_k, n_b, heads, dh;
+    int packed;        // 0: rows along i; >0: sequences per tile (T = n_k)
+    int row_tiles;     // query tiles along the tiled axis
+    int n_kv;          // KV tiles per problem
+    float scale_log2;  // scale * log2(e)
+    __nv_bfloat16* o;
+    int64_t o_sa, o_sb, o_si;
+};
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred done;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra WAIT_%=;\n}" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2, int c3, int c4) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+#define PAB_TMEM_LD32(taddr, r)                                                                              \
+    asm volatile(                                                                                            \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"    \
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                           \
+        : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7]),    \
+          "=f"(r[8]), "=f"(r[9]), "=f"(r[10]), "=f"(r[11]), "=f"(r[12]), "=f"(r[13]), "=f"(r[14]),          \
+          "=f"(r[15]), "=f"(r[16]), "=f"(r[17]), "=f"(r[18]), "=f"(r[19]), "=f"(r[20]), "=f"(r[21]),        \
+          "=f"(r[22]), "=f"(r[23]), "=f"(r[24]), "=f"(r[25]), "=f"(r[26]), "=f"(r[27]), "=f"(r[28]),        \
+          "=f"(r[29]), "=f"(r[30]), "=f"(r[31])                                                              \
+        : "r"(taddr))
+
+#define PAB_TMEM_LD16(taddr, r)                                                                              \
+    asm volatile(                                                                                            \
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"   \
+        " [%16];"                                                                                            \
+        : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7]),    \
+          "=f"(r[8]), "=f"(r[9]), "=f"(r[10]), "=f"(r[11]), "=f"(r[12]), "=f"(r[13]), "=f"(r[14]),          \
+          "=f"(r[15])                                                                                        \
+        : "r"(taddr))
+
+#define PAB_TMEM_ST16(taddr, r)                                                                              \
+    asm volatile(                                                                                            \
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15," \
+        "%16};" ::"r"(taddr),                                                                                \
+        "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7]), "f"(r[8]),   \
+        "f"(r[9]), "f"(r[10]), "f"(r[11]), "f"(r[12]), "f"(r[13]), "f"(r[14]), "f"(r[15])                    \
+        : "memory")
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// ------------------------------------------------------ UMMA descriptors
+// Shared-memory matrix descriptor (sm_100): start>>4 [0,14), LBO>>4 [16,30),
+// SBO>>4 [32,46), version=1 [46,48), base offset [49,52), layout [61,64).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)layout << 61;
+    return d;
+}
+constexpr uint32_t kLayoutSW128 = 2, kLayoutSW32 = 6;
+
+// Instruction descriptor, kind::f16: D=f32 [4,6)=1, A=bf16 [7,10)=1, B=bf16 [10,13)=1,
+// A major [15], B major [16] (0 = K-major, 1 = MN-major), N>>3 [17,23), M>>4 [24,29).
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int b_mn_major) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(M >> 4) << 24);
+}
+
+// ------------------------------------------------------------- the kernel
+template <int N128, int N32>
+struct Geometry {
+    static constexpr int kDhPad = 64 * N128 + 16 * N32;
+    static constexpr int kTileBytes = N128 * 16384 + N32 * 4096;  // one 128-row operand tile
+    static constexpr int kQ0 = 0;
+    static constexpr int kK0 = 2 * kTileBytes;     // 2 K stages
+    static constexpr int kV0 = 4 * kTileBytes;     // 2 V stages
+    static constexpr int kP0 = 6 * kTileBytes;     // 2 P tiles
+    static constexpr int kBar = kP0 + 2 * kPBytes;
+    static constexpr int kSmem = kBar + 256 + 1024;  // + barriers + alignment slack
+};
+
+struct Bars {
+    uint64_t q_full, kv_full[2], v_full[2], kv_empty[2], s_full[2], s_free[2], p_full[2], o_done[2];
+    uint32_t tmem_base;
+};
+
+template <int N128, int N32>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap q128, const __grid_constant__ CUtensorMap q32,
+                   const __grid_constant__ CUtensorMap k128, const __grid_constant__ CUtensorMap k32,
+                   const __grid_constant__ CUtensorMap v128, const __grid_constant__ CUtensorMap v32,
+                   const Params p) {
+    using G = Geometry<N128, N32>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    Bars* bars = reinterpret_cast<Bars*>(smem + G::kBar);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pair = blockIdx.x, h = blockIdx.y, az = blockIdx.z;
+    // problem coordinates of the two query tiles
+    int a_idx, b_idx0, i_base[2], b_base[2];
+    if (p.packed) {
+        a_idx = az;
+        b_idx0 = 0;
+        for (int t = 0; t < 2; ++t) {
+            b_base[t] = (2 * pair + t) * p.packed;
+            i_base[t] = 0;
+        }
+    } else {
+        a_idx = az / p.n_b;
+        b_idx0 = az - a_idx * p.n_b;
+        for (int t = 0; t < 2; ++t) {
+            b_base[t] = b_idx0;
+            i_base[t] = (2 * pair + t) * kRows;
+        }
+    }
+    const int box_rows = p.packed ? p.packed * p.n_k : kRows;  // rows a TMA box fills
+    const uint32_t box_bytes = (uint32_t)box_rows * (uint32_t)(N128 * 128 + N32 * 32);
+
+    // ---------------------------------------------------------------- setup
+    if (warp == 8 && lane == 0) {
+        prefetch_map(&q128); prefetch_map(&k128); prefetch_map(&v128);
+        if (N32) { prefetch_map(&q32); prefetch_map(&k32); prefetch_map(&v32); }
+        mbar_init(&bars->q_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bars->kv_full[s], 1);
+            mbar_init(&bars->v_full[s], 1);
+            mbar_init(&bars->kv_empty[s], 1);
+            mbar_init(&bars->s_full[s], 1);
+            mbar_init(&bars->s_free[s], kRows);
+            mbar_init(&bars->p_full[s], kRows);
+            mbar_init(&bars->o_done[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 9) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&bars->tmem_base)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (box_rows < kRows) {
+        // packed tiles leave rows [box_rows, 128) of Q/K/V untouched by TMA:
+        // zero them once so masked lanes can never inject NaN/Inf into P.V
+        uint4 zero = make_uint4(0, 0, 0, 0);
+        for (int off = threadIdx.x * 16; off < 6 * G::kTileBytes; off += kThreads * 16)
+            *reinterpret_cast<uint4*>(smem + off) = zero;
+        fence_async_smem();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bars->tmem_base;
+    const int n_kv = p.n_kv;
+
+    if (warp == 8) {
+        // ===================================================== TMA producer
+        if (lane == 0) {
+            mbar_expect_tx(&bars->q_full, 2 * box_bytes);
+            for (int t = 0; t < 2; ++t) {
+                uint8_t* dst = smem + G::kQ0 + t * G::kTileBytes;
+                for (int blk = 0; blk < N128; ++blk)
+                    tma_load_5d(dst + blk * 16384, &q128, &bars->q_full, 64 * blk, h, i_base[t], b_base[t], a_idx);
+                for (int blk = 0; blk < N32; ++blk)
+                    tma_load_5d(dst + N128 * 16384 + blk * 4096, &q32, &bars->q_full, 64 * N128 + 16 * blk, h,
+                                i_base[t], b_base[t], a_idx);
+            }
+            for (int j = 0; j < n_kv; ++j) {
+                const int st = j & 1;
+                if (j >= 2) mbar_wait(&bars->kv_empty[st], ((j >> 1) - 1) & 1);
+                const int kv_i = p.packed ? 0 : j * kKv;
+                // packed mode: each query tile owns its sequences, so KV tile j
+                // (j < 2) holds the keys of query tile j
+                const int kv_b_eff = p.packed ? b_base[j] : b_idx0;
+                uint8_t* kd = smem + G::kK0 + st * G::kTileBytes;
+                uint8_t* vd = smem + G::kV0 + st * G::kTileBytes;
+                mbar_expect_tx(&bars->kv_full[st], box_bytes);
+                for (int blk = 0; blk < N128; ++blk)
+                    tma_load_5d(kd + blk * 16384, &k128, &bars->kv_full[st], 64 * blk, h, kv_i, kv_b_eff, a_idx);
+                for (int blk = 0; blk < N32; ++blk)
+                    tma_load_5d(kd + N128 * 16384 + blk * 4096, &k32, &bars->kv_full[st], 64 * N128 + 16 * blk, h,
+                                kv_i, kv_b_eff, a_idx);
+                mbar_expect_tx(&bars->v_full[st], box_bytes);
+                for (int blk = 0; blk < N128; ++blk)
+                    tma_load_5d(vd + blk * 16384, &v128, &bars->v_full[st], 64 * blk, h, kv_i, kv_b_eff, a_idx);
+                for (int blk = 0; blk < N32; ++blk)
+                    tma_load_5d(vd + N128 * 16384 + blk * 4096, &v32, &bars->v_full[st], 64 * N128 + 16 * blk, h,
+                                kv_i, kv_b_eff, a_idx);
+            }
+        }
+    } else if (warp == 9) {
+        // ====================================================== MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idS = idesc_bf16(128, 128, 0);
+            constexpr uint32_t idO64 = idesc_bf16(128, 64, 1);
+            constexpr uint32_t idO16 = idesc_bf16(128, 16, 1);
+            const uint32_t q_addr = smem_u32(smem + G::kQ0);
+            const uint32_t k_addr = smem_u32(smem + G::kK0);
+            const uint32_t v_addr = smem_u32(smem + G::kV0);
+            const uint32_t p_addr = smem_u32(smem + G::kP0);
+            mbar_wait(&bars->q_full, 0);
+            tc_fence_after();
+            // S_t = Q_t K^T over the dh K-blocks
+            auto issue_s = [&](int t, int st) {
+                const uint32_t qa = q_addr + t * G::kTileBytes, ka = k_addr + st * G::kTileBytes;
+                const uint32_t d = tmem + 128 * t;
+                uint32_t acc = 0;
+                for (int blk = 0; blk < N128; ++blk)
+                    for (int k = 0; k < 4; ++k) {
+                        tc_mma(d, smem_desc(qa + blk * 16384 + 32 * k, 16, 1024, kLayoutSW128),
+                               smem_desc(ka + blk * 16384 + 32 * k, 16, 1024, kLayoutSW128), idS, acc);
+                        acc = 1;
+                    }
+                for (int blk = 0; blk < N32; ++blk) {
+                    tc_mma(d, smem_desc(qa + N128 * 16384 + blk * 4096, 16, 256, kLayoutSW32),
+                           smem_desc(ka + N128 * 16384 + blk * 4096, 16, 256, kLayoutSW32), idS, acc);
+                    acc = 1;
+                }
+            };
+            // O_t += P_t V over 8 K-steps of 16 keys, per 64- / 16-wide dh block
+            auto issue_pv = [&](int t, int st, uint32_t accumulate) {
+                const uint32_t pa = p_addr + t * kPBytes, va = v_addr + st * G::kTileBytes;
+                const uint32_t d = tmem + 256 + 128 * t;
+                for (int k = 0; k < kKv / 16; ++k) {
+                    const uint64_t a_desc = smem_desc(pa + (k >> 2) * 16384 + 32 * (k & 3), 16, 1024, kLayoutSW128);
+                    const uint32_t acc = (accumulate || k > 0) ? 1u : 0u;
+                    for (int blk = 0; blk < N128; ++blk)
+                        tc_mma(d + 64 * blk, a_desc, smem_desc(va + blk * 16384 + 2048 * k, 16, 1024, kLayoutSW128),
+                               idO64, acc);
+                    for (int blk = 0; blk < N32; ++blk)
+                        tc_mma(d + 64 * N128 + 16 * blk, a_desc,
+                               smem_desc(va + N128 * 16384 + blk * 4096 + 512 * k, 16, 256, kLayoutSW32), idO16,
+                               acc);
+                }
+            };
+            if (p.packed) {
+                // two independent single-tile problems: tile t uses KV stage t
+                for (int t = 0; t < 2; ++t) {
+                    mbar_wait(&bars->kv_full[t], 0);
+                    tc_fence_after();
+                    issue_s(t, t);
+                    tc_commit(&bars->s_full[t]);
+                }
+                for (int t = 0; t < 2; ++t) {
+                    mbar_wait(&bars->v_full[t], 0);
+                    mbar_wait(&bars->p_full[t], 0);
+                    tc_fence_after();
+                    issue_pv(t, t, 0);
+                    tc_commit(&bars->o_done[t]);
+                }
+            } else {
+                mbar_wait(&bars->kv_full[0], 0);
+                tc_fence_after();
+                issue_s(0, 0);
+                tc_commit(&bars->s_full[0]);
+                issue_s(1, 0);
+                tc_commit(&bars->s_full[1]);
+                for (int j = 0; j < n_kv; ++j) {
+                    const int st = j & 1;
+                    const uint32_t ph = (j >> 1) & 1;
+                    mbar_wait(&bars->v_full[st], ph);
+                    for (int t = 0; t < 2; ++t) {
+                        mbar_wait(&bars->p_full[t], j & 1);
+                        tc_fence_after();
+                        issue_pv(t, st, j > 0);
+                        tc_commit(&bars->o_done[t]);
+                        if (j + 1 < n_kv) {
+                            const int st1 = (j + 1) & 1;
+                            if (t == 0) {
+                                mbar_wait(&bars->kv_full[st1], ((j + 1) >> 1) & 1);
+                            }
+                            mbar_wait(&bars->s_free[t], j & 1);
+                            tc_fence_after();
+                            issue_s(t, st1);
+                            tc_commit(&bars->s_full[t]);
+                        }
+                    }
+                    tc_commit(&bars->kv_empty[st]);
+                }
+            }
+        }
+    } else {
+        // ================================================= softmax groups
+        const int t = warp >> 2;            // query tile of this group
+        const int wl = warp & 3;            // TMEM lane quarter
+        const int row = wl * 32 + lane;     // tile row owned by this thread
+        const uint32_t lane_off = (uint32_t)(wl * 32) << 16;
+        const uint32_t s_tmem = tmem + lane_off + 128 * t;
+        const uint32_t o_tmem = tmem + lane_off + 256 + 128 * t;
+        uint8_t* p_tile = smem + G::kP0 + t * kPBytes;
+        const int T = p.n_k;
+        const int group = p.packed ? row / T : 0;
+        const int n_iter = p.packed ? 1 : n_kv;
+        float m_run = -INFINITY, l_run = 0.f;
+
+        for (int j = 0; j < n_iter; ++j) {
+            mbar_wait(&bars->s_full[t], j & 1);
+            tc_fence_after();
+            float s[kKv];
+            PAB_TMEM_LD32(s_tmem + 0, (s + 0));
+            PAB_TMEM_LD32(s_tmem + 32, (s + 32));
+            PAB_TMEM_LD32(s_tmem + 64, (s + 64));
+            PAB_TMEM_LD32(s_tmem + 96, (s + 96));
+            tmem_wait_ld();
+            tc_fence_before();
+            mbar_arrive(&bars->s_free[t]);
+
+            // mask + tile max, in the log2 domain
+            float m_tile = -INFINITY;
+            if (p.packed) {
+                const int lo = group * T, hi = lo + T;
+#pragma unroll
+                for (int c = 0; c < kKv; ++c) {
+                    const bool ok = (c >= lo) && (c < hi);
+                    s[c] = ok ? s[c] * p.scale_log2 : -INFINITY;
+                    m_tile = fmaxf(m_tile, s[c]);
+                }
+            } else {
+                const int valid = p.n_k - j * kKv;
+#pragma unroll
+                for (int c = 0; c < kKv; ++c) {
+                    s[c] = (c < valid) ? s[c] * p.scale_log2 : -INFINITY;
+                    m_tile = fmaxf(m_tile, s[c]);
+                }
+            }
+            // previous P.V must be finished before P smem is overwritten or O rescaled
+            if (j > 0) {
+                mbar_wait(&bars->o_done[t], (j - 1) & 1);
+                tc_fence_after();
+            }
+            const bool need = m_tile > m_run + 8.0f;
+            if (__any_sync(0xffffffffu, need)) {
+                const float m_new = fmaxf(m_run, m_tile);
+                if (j > 0) {
+                    const float alpha = fast_exp2(m_run - m_new);
+                    l_run *= alpha;
+#pragma unroll
+                    for (int c0 = 0; c0 < G::kDhPad; c0 += 16) {
+                        float o[16];
+                        PAB_TMEM_LD16(o_tmem + c0, o);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) o[e] *= alpha;
+                        PAB_TMEM_ST16(o_tmem + c0, o);
+                    }
+                    tmem_wait_st();
+                }
+                m_run = m_new;
+            }
+            const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+            // P = exp2(s - m), row sum, bf16 pack into the 128B-swizzled K-major tile
+            float sum = 0.f;
+            const uint32_t rsw = (uint32_t)(row & 7);
+#pragma unroll
+            for (int chunk = 0; chunk < kKv / 8; ++chunk) {
+                uint32_t packed4[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float x0 = fast_exp2(s[chunk * 8 + 2 * e] - m_use);
+                    const float x1 = fast_exp2(s[chunk * 8 + 2 * e + 1] - m_use);
+                    sum += x0 + x1;
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(x0, x1);
+                    packed4[e] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+                const int blk = chunk >> 3, cw = chunk & 7;
+                uint8_t* dst = p_tile + blk * 16384 + row * 128 + ((cw ^ rsw) << 4);
+                *reinterpret_cast<uint4*>(dst) = make_uint4(packed4[0], packed4[1], packed4[2], packed4[3]);
+            }
+            l_run += sum;
+            fence_async_smem();
+            tc_fence_before();
+            mbar_arrive(&bars->p_full[t]);
+        }
+
+        // ------------------------------------------------------ epilogue
+        mbar_wait(&bars->o_done[t], (n_iter - 1) & 1);
+        tc_fence_after();
+        bool store = false;
+        __nv_bfloat16* dst = nullptr;
+        if (p.packed) {
+            const int b = b_base[t] + group, i = row - group * T;
+            store = (group < p.packed) && (b < p.n_b) && (i < T);
+            dst = p.o + (int64_t)a_idx * p.o_sa + (int64_t)b * p.o_sb + (int64_t)i * p.o_si + (int64_t)h * p.dh;
+        } else {
+            const int i = i_base[t] + row;
+            store = i < p.n_q;
+            dst = p.o + (int64_t)a_idx * p.o_sa + (int64_t)b_base[t] * p.o_sb + (int64_t)i * p.o_si +
+                  (int64_t)h * p.dh;
+        }
+        const float inv = (l_run > 0.f) ? 1.0f / l_run : 0.f;
+#pragma unroll
+        for (int c0 = 0; c0 < G::kDhPad; c0 += 16) {
+            float o[16];
+            PAB_TMEM_LD16(o_tmem + c0, o);
+            tmem_wait_ld();
+            if (store) {
+#pragma unroll
+                for (int e = 0; e < 16; e += 8) {
+                    if (c0 + e < p.dh) {
+                        uint32_t w[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            __nv_bfloat162 b2 = __floats2bfloat162_rn(o[e + 2 * q] * inv, o[e + 2 * q + 1] * inv);
+                            w[q] = *reinterpret_cast<uint32_t*>(&b2);
+                        }
+                        *reinterpret_cast<uint4*>(dst + c0 + e) = make_uint4(w[0], w[1], w[2], w[3]);
+                    }
+                }
+            }
+        }
+        tc_fence_before();
+    }
+    __syncthreads();
+    if (warp == 9) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    }
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    });
+    return fn;
+}
+
+// 5-D view (dh, heads, i, b, a) of one operand; box = (inner, 1, rows_i, rows_b, 1)
+bool make_map(CUtensorMap* map, const void* base, int dh, int heads, int n_i, int n_b, int n_a, int64_t s_i,
+              int64_t s_b, int64_t s_a, int box_inner, int box_i, int box_b, CUtensorMapSwizzle swz) {
+    auto encode = get_encode();
+    if (!encode) return false;
+    cuuint64_t dims[5] = {(cuuint64_t)dh, (cuuint64_t)heads, (cuuint64_t)n_i, (cuuint64_t)n_b, (cuuint64_t)n_a};
+    auto bytes = [](int64_t s) { return (cuuint64_t)(s > 0 ? s * 2 : 16); };
+    cuuint64_t strides[4] = {(cuuint64_t)dh * 2, bytes(s_i), bytes(s_b), bytes(s_a)};
+    cuuint32_t box[5] = {(cuuint32_t)box_inner, 1, (cuuint32_t)box_i, (cuuint32_t)box_b, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int N128, int N32>
+int launch(const pab_attn_args* a, int packed, cudaStream_t st) {
+    using G = Geometry<N128, N32>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(attn_tc_kernel<N128, N32>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem) !=
+            cudaSuccess)
+            return launch_status("attn_tc smem attribute");
+        attr_set = true;
+    }
+    const int box_i = packed ? a->n_k : kRows;
+    const int box_b = packed ? packed : 1;
+    CUtensorMap maps[6];
+    struct Op { const void* ptr; int64_t sa, sb, si; int n_i; } ops[3] = {
+        {a->q, a->q_sa, a->q_sb, a->q_si, a->n_q}, {a->k, a->k_sa, a->k_sb, a->k_si, a->n_k},
+        {a->v, a->v_sa, a->v_sb, a->v_si, a->n_k}};
+    for (int o = 0; o < 3; ++o) {
+        const Op& op = ops[o];
+        if (!make_map(&maps[2 * o], op.ptr, a->dh, a->heads, op.n_i, a->n_b, a->n_a, op.si, op.sb, op.sa,
+                      N128 ? 64 : 16, box_i, box_b, N128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B))
+            return PAB_ERR_CUDA;
+        if (!make_map(&maps[2 * o + 1], op.ptr, a->dh, a->heads, op.n_i, a->n_b, a->n_a, op.si, op.sb, op.sa, 16,
+                      box_i, box_b, CU_TENSOR_MAP_SWIZZLE_32B))
+            return PAB_ERR_CUDA;
+    }
+    Params p;
+    p.n_q = a->n_q; p.n_k = a->n_k; p.n_b = a->n_b; p.heads = a->heads; p.dh = a->dh;
+    p.packed = packed;
+    p.scale_log2 = a->scale * 1.4426950408889634f;
+    p.o = reinterpret_cast<__nv_bfloat16*>(a->o);
+    p.o_sa = a->o_sa; p.o_sb = a->o_sb; p.o_si = a->o_si;
+    dim3 grid;
+    if (packed) {
+        p.row_tiles = (a->n_b + packed - 1) / packed;
+        p.n_kv = 2;  // one KV tile per query tile
+        grid = dim3((unsigned)((p.row_tiles + 1) / 2), (unsigned)a->heads, (unsigned)a->n_a);
+    } else {
+        p.row_tiles = (a->n_q + kRows - 1) / kRows;
+        p.n_kv = (a->n_k + kKv - 1) / kKv;
+        grid = dim3((unsigned)((p.row_tiles + 1) / 2), (unsigned)a->heads, (unsigned)((int64_t)a->n_a * a->n_b));
+    }
+    attn_tc_kernel<N128, N32><<<grid, kThreads, G::kSmem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4],
+                                                                 maps[5], p);
+    return launch_status("attn_tc");
+}
+
+int packing_for(const pab_attn_args* a) {
+    if (a->n_b > 1 && a->n_q == a->n_k && a->n_k <= 64) return kRows / a->n_k;
+    return 0;
+}
+
+}  // namespace tc
+
+bool attn_tc_supported(const pab_attn_args* a) {
+    if (a->dh % 8 != 0 || a->dh > 96 || a->n_k < 1) return false;
+    const int64_t strides[] = {a->q_sa, a->q_sb, a->q_si, a->k_sa, a->k_sb, a->k_si,
+                               a->v_sa, a->v_sb, a->v_si, a->o_si};
+    for (int64_t s : strides)
+        if (s % 8 != 0 || s < 0) return false;
+    const uintptr_t ptrs[] = {(uintptr_t)a->q, (uintptr_t)a->k, (uintptr_t)a->v, (uintptr_t)a->o};
+    for (uintptr_t p : ptrs)
+        if (p % 16 != 0) return false;
+    if ((int64_t)a->n_a * a->n_b > 65535 || a->heads > 65535) return false;
+    if (a->n_a > 0x7fffffff || a->n_q > (1 << 30)) return false;
+    return tc::get_encode() != nullptr;
+}
+
+int attn_tc_launch(const pab_attn_args* a, cudaStream_t st) {
+    const int packed = tc::packing_for(a);
+    const int n128 = a->dh / 64;
+    const int n32 = (a->dh - 64 * n128 + 15) / 16;
+#define PAB_TC(A, B) \
+    if (n128 == A && n32 == B) return tc::launch<A, B>(a, packed, st)
+    PAB_TC(0, 1); PAB_TC(0, 2); PAB_TC(0, 3);
+    PAB_TC(1, 0); PAB_TC(1, 1); PAB_TC(1, 2);
+#undef PAB_TC
+    return PAB_ERR_UNSUPPORTED;
+}
+
+}  // namespace pab

@@ -1,0 +1,300 @@
+// HBM-bound kernels of the PAB step: the broadcast epilogue with its
+// modulated-LayerNorm prologue (K4+K5), GELU (K7), the fused CFG + DDIM
+// update (K8) and the on-device splitmix64 parameter fill.
+//
+// All of them stream their operands exactly once with 16-byte (fp32x4) /
+// 8-byte (bf16x4) vector accesses; one warp owns one row for the row-wise
+// LayerNorm so the reduction never leaves registers.
+#include "common.cuh"
+#include <math.h>
+
+namespace pab {
+
+// --------------------------------------------------------------------------
+// K4+K5: x_out = x_in + sum(pending); h = modnorm(x_out) | bf16(x_out)
+// reference: model.py:317-324 (_modulated_norm), model.py:503 (x + o),
+//            numerics.py:115-130 (layer_norm, population variance, eps)
+// --------------------------------------------------------------------------
+template <int VEC>
+struct VecT;
+template <>
+struct VecT<4> {
+    __device__ static void load_f32(const float* p, float* v) {
+        float4 t = *reinterpret_cast<const float4*>(p);
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    }
+    __device__ static void store_f32(float* p, const float* v) {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    __device__ static void add_bf16(const __nv_bfloat16* p, float* v) {
+        uint2 raw = *reinterpret_cast<const uint2*>(p);
+        __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162*>(&raw.x);
+        __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&raw.y);
+        float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+        v[0] += fa.x; v[1] += fa.y; v[2] += fb.x; v[3] += fb.y;
+    }
+    __device__ static void store_bf16(__nv_bfloat16* p, const float* v) {
+        __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]);
+        __nv_bfloat162 b = __floats2bfloat162_rn(v[2], v[3]);
+        uint2 raw;
+        raw.x = *reinterpret_cast<uint32_t*>(&a);
+        raw.y = *reinterpret_cast<uint32_t*>(&b);
+        *reinterpret_cast<uint2*>(p) = raw;
+    }
+};
+template <>
+struct VecT<1> {
+    __device__ static void load_f32(const float* p, float* v) { v[0] = *p; }
+    __device__ static void store_f32(float* p, const float* v) { *p = v[0]; }
+    __device__ static void add_bf16(const __nv_bfloat16* p, float* v) { v[0] += __bfloat162float(*p); }
+    __device__ static void store_bf16(__nv_bfloat16* p, const float* v) { *p = __float2bfloat16_rn(v[0]); }
+};
+
+template <int VEC, int NV>
+__global__ void __launch_bounds__(256) residual_modnorm_kernel(
+    const float* __restrict__ x_in, float* __restrict__ x_out, PendingList pend,
+    const float* __restrict__ gamma, const float* __restrict__ beta,
+    const float* __restrict__ mod, __nv_bfloat16* __restrict__ h_out,
+    int64_t rows, int D, float eps, int mode, int write_x) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (row >= rows) return;
+    const int64_t base = row * (int64_t)D;
+    float v[NV][VEC];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        const int c = (j * 32 + lane) * VEC;
+        if (c < D) {
+            VecT<VEC>::load_f32(x_in + base + c, v[j]);
+#pragma unroll
+            for (int p = 0; p < PAB_MAX_PENDING; ++p)
+                if (p < pend.n) VecT<VEC>::add_bf16(pend.p[p] + base + c, v[j]);
+            if (write_x) VecT<VEC>::store_f32(x_out + base + c, v[j]);
+        }
+    }
+    if (mode == 0) return;
+    if (mode == 2) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            const int c = (j * 32 + lane) * VEC;
+            if (c < D) VecT<VEC>::store_bf16(h_out + base + c, v[j]);
+        }
+        return;
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        const int c = (j * 32 + lane) * VEC;
+        if (c < D) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) s += v[j][e];
+        }
+    }
+    const float mean = warp_sum(s) / (float)D;
+    float q = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        const int c = (j * 32 + lane) * VEC;
+        if (c < D) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+                v[j][e] -= mean;
+                q += v[j][e] * v[j][e];
+            }
+        }
+    }
+    const float var = warp_sum(q) / (float)D;
+    const float inv = 1.0f / sqrtf(var + eps);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        const int c = (j * 32 + lane) * VEC;
+        if (c < D) {
+            float o[VEC];
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+                float h = v[j][e] * inv;
+                if (gamma) h = h * gamma[c + e] + beta[c + e];
+                o[e] = h * (1.0f + mod[D + c + e]) + mod[c + e];
+            }
+            VecT<VEC>::store_bf16(h_out + base + c, o);
+        }
+    }
+}
+
+template <int VEC>
+static int launch_modnorm_vec(const float* x_in, float* x_out, const PendingList& pl,
+                              const float* gamma, const float* beta, const float* mod,
+                              __nv_bfloat16* h, int64_t rows, int D, float eps, int mode,
+                              int write_x, cudaStream_t st) {
+    const int per_lane = (D + 32 * VEC - 1) / (32 * VEC);
+    const int warps = 8;
+    dim3 grid((unsigned)((rows + warps - 1) / warps)), block(32 * warps);
+#define PAB_MN(NVV)                                                                       \
+    residual_modnorm_kernel<VEC, NVV><<<grid, block, 0, st>>>(x_in, x_out, pl, gamma, beta, \
+                                                              mod, h, rows, D, eps, mode, write_x)
+    if (per_lane <= 1) PAB_MN(1);
+    else if (per_lane <= 2) PAB_MN(2);
+    else if (per_lane <= 4) PAB_MN(4);
+    else if (per_lane <= 8) PAB_MN(8);
+    else if (per_lane <= 9) PAB_MN(9);
+    else if (per_lane <= 12) PAB_MN(12);
+    else if (per_lane <= 16) PAB_MN(16);
+    else return PAB_ERR_UNSUPPORTED;
+#undef PAB_MN
+    return launch_status("residual_modnorm");
+}
+
+// --------------------------------------------------------------------------
+// K8: end-of-step drain + CFG + DDIM (diffusion.py:100-103, 183-189)
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) ddim_cfg_kernel(
+    float* __restrict__ z, const float* __restrict__ r, PendingList pend, int batch,
+    int64_t n, int guidance, float g, float c_noise, float c_signal, float c_next_sig,
+    float c_next_noise) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float eps[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        if (b >= batch) break;
+        float e = r[(int64_t)b * n + i];
+#pragma unroll
+        for (int p = 0; p < PAB_MAX_PENDING; ++p)
+            if (p < pend.n) e = __fadd_rn(e, __bfloat162float(pend.p[p][(int64_t)b * n + i]));
+        eps[b] = e;
+    }
+    if (guidance) {
+        // eps_u + g * (eps_c - eps_u), conditional half first (diffusion.py:183-186)
+        const float eh = __fadd_rn(eps[1], __fmul_rn(g, __fsub_rn(eps[0], eps[1])));
+#pragma unroll
+        for (int b = 0; b < 8; ++b) eps[b] = eh;
+    }
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        if (b >= batch) break;
+        const int64_t k = (int64_t)b * n + i;
+        const float x0 = __fdiv_rn(__fsub_rn(z[k], __fmul_rn(c_noise, eps[b])), c_signal);
+        z[k] = __fadd_rn(__fmul_rn(c_next_sig, x0), __fmul_rn(c_next_noise, eps[b]));
+    }
+}
+
+// --------------------------------------------------------------------------
+// K7: tanh-approximate GELU, bf16 in/out, 8 elements per thread
+// --------------------------------------------------------------------------
+__device__ __forceinline__ float gelu_tanh(float x) {
+    const float k0 = 0.7978845608028654f;  // sqrt(2/pi)
+    const float inner = k0 * (x + 0.044715f * (x * x * x));
+    // tanh(u) = 1 - 2 / (exp(2u) + 1); exact to ~1e-7 relative, far below bf16 output rounding
+    const float t = 1.0f - __fdividef(2.0f, __expf(2.0f * inner) + 1.0f);
+    return 0.5f * x * (1.0f + t);
+}
+
+__global__ void __launch_bounds__(256) gelu_kernel(const __nv_bfloat16* __restrict__ in,
+                                                   __nv_bfloat16* __restrict__ out, int64_t n) {
+    const int64_t i8 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    if (i8 + 8 <= n) {
+        uint4 raw = *reinterpret_cast<const uint4*>(in + i8);
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float2 f = __bfloat1622float2(h[j]);
+            h[j] = __floats2bfloat162_rn(gelu_tanh(f.x), gelu_tanh(f.y));
+        }
+        *reinterpret_cast<uint4*>(out + i8) = raw;
+    } else {
+        for (int64_t i = i8; i < n; ++i) out[i] = __float2bfloat16_rn(gelu_tanh(__bfloat162float(in[i])));
+    }
+}
+
+// --------------------------------------------------------------------------
+// splitmix64 fill (numerics.py:161-201; model.py:176-182)
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix_out(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void fill_uniform_kernel(void* dst, int dtype, int64_t rows, int64_t cols, int64_t ld,
+                                    int64_t col0, uint64_t state, uint64_t first, double lo,
+                                    double span) {
+    const int64_t total = rows * cols;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = first + (uint64_t)i + 1ull;
+        const uint64_t mant = splitmix_out(state + k * 0x9E3779B97F4A7C15ull) >> 11;
+        const double u = (double)mant * 1.1102230246251565e-16;  // 2^-53, exact
+        const float v = __double2float_rn(__dadd_rn(lo, __dmul_rn(u, span)));
+        const int64_t r = i / cols, c = i - r * cols;
+        const int64_t o = r * ld + col0 + c;
+        if (dtype == 0) reinterpret_cast<float*>(dst)[o] = v;
+        else reinterpret_cast<__nv_bfloat16*>(dst)[o] = __float2bfloat16_rn(v);
+    }
+}
+
+}  // namespace pab
+
+using namespace pab;
+
+extern "C" int pab_residual_modnorm(const float* x_in, float* x_out, const void* const* pending,
+                                    int n_pending, const float* gamma, const float* beta,
+                                    const float* mod, void* h_out, int64_t rows, int D, float eps,
+                                    int mode, void* stream) {
+    if (rows < 0 || D <= 0 || n_pending < 0 || n_pending > PAB_MAX_PENDING) return PAB_ERR_SHAPE;
+    if (mode < 0 || mode > 2) return PAB_ERR_INVALID;
+    if (mode == 1 && mod == nullptr) return PAB_ERR_INVALID;
+    if (mode != 0 && h_out == nullptr) return PAB_ERR_INVALID;
+    if ((gamma == nullptr) != (beta == nullptr)) return PAB_ERR_INVALID;
+    if (rows == 0) return PAB_OK;
+    const int write_x = (n_pending > 0 || x_in != x_out) ? 1 : 0;
+    if (mode == 0 && !write_x) return PAB_OK;
+    PendingList pl = make_pending(pending, n_pending);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    auto* h = reinterpret_cast<__nv_bfloat16*>(h_out);
+    bool aligned = (D % 4 == 0) && ((uintptr_t)x_in % 16 == 0) && ((uintptr_t)x_out % 16 == 0) &&
+                   (h == nullptr || (uintptr_t)h % 8 == 0);
+    for (int i = 0; i < n_pending; ++i) aligned = aligned && ((uintptr_t)pending[i] % 8 == 0);
+    if (aligned) return launch_modnorm_vec<4>(x_in, x_out, pl, gamma, beta, mod, h, rows, D, eps, mode, write_x, st);
+    return launch_modnorm_vec<1>(x_in, x_out, pl, gamma, beta, mod, h, rows, D, eps, mode, write_x, st);
+}
+
+extern "C" int pab_ddim_cfg(float* z, const float* r, const void* const* pending, int n_pending,
+                            int batch, int64_t n, int guidance, double guidance_scale,
+                            double a_cur, double a_next, void* stream) {
+    if (batch < 1 || batch > 8 || n < 0 || n_pending < 0 || n_pending > PAB_MAX_PENDING) return PAB_ERR_SHAPE;
+    if (guidance && batch != 2) return PAB_ERR_SHAPE;
+    if (!(a_cur > 0.0) || a_cur > 1.0 || a_next < 0.0 || a_next > 1.0) return PAB_ERR_INVALID;
+    if (n == 0) return PAB_OK;
+    PendingList pl = make_pending(pending, n_pending);
+    const float c_noise = (float)sqrt(1.0 - a_cur), c_signal = (float)sqrt(a_cur);
+    const float c_next_sig = (float)sqrt(a_next), c_next_noise = (float)sqrt(1.0 - a_next);
+    dim3 block(256), grid((unsigned)((n + 255) / 256));
+    ddim_cfg_kernel<<<grid, block, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        z, r, pl, batch, n, guidance, (float)guidance_scale, c_noise, c_signal, c_next_sig, c_next_noise);
+    return launch_status("ddim_cfg");
+}
+
+extern "C" int pab_gelu_bf16(const void* in, void* out, int64_t n, void* stream) {
+    if (n < 0) return PAB_ERR_SHAPE;
+    if (n == 0) return PAB_OK;
+    if ((uintptr_t)in % 16 || (uintptr_t)out % 16) return PAB_ERR_UNSUPPORTED;
+    const int64_t threads = (n + 7) / 8;
+    dim3 block(256), grid((unsigned)((threads + 255) / 256));
+    gelu_kernel<<<grid, block, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const __nv_bfloat16*>(in), reinterpret_cast<__nv_bfloat16*>(out), n);
+    return launch_status("gelu");
+}
+
+extern "C" int pab_fill_uniform(void* dst, int dtype, int64_t rows, int64_t cols, int64_t ld,
+                                int64_t col0, uint64_t state, uint64_t first_draw, double lo,
+                                double hi, void* stream) {
+    if (rows < 0 || cols < 0 || ld < col0 + cols || (dtype != 0 && dtype != 1)) return PAB_ERR_SHAPE;
+    if (!(lo < hi)) return PAB_ERR_INVALID;
+    if (rows * cols == 0) return PAB_OK;
+    const int64_t total = rows * cols;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 64) blocks = 148 * 64;
+    fill_uniform_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        dst, dtype, rows, cols, ld, col0, state, first_draw, lo, hi - lo);
+    return launch_status("fill_uniform");
+}

@@ -1,0 +1,137 @@
+"""Thin torch-tensor wrappers over the C ABI (device memory owned by torch).
+
+Every wrapper launches on torch's current CUDA stream and validates the
+tensors it hands to the library (device, dtype, contiguity); shape errors are
+raised as the reference's ShapeError kinds.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import torch
+
+from . import _lib
+from .errors import ShapeError, ValidationError
+
+MAX_PENDING = _lib.MAX_PENDING
+IMPL_AUTO, IMPL_TCGEN05, IMPL_SIMT = 0, 1, 2
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _need(t: torch.Tensor, dtype, name: str):
+    if not t.is_cuda:
+        raise ValidationError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValidationError(f"{name} must be {dtype}, got {t.dtype}")
+
+
+def residual_modnorm(x_in, x_out, pending, h_out=None, mod=None, gamma=None, beta=None, mode=1, eps=1e-5):
+    """x_out = x_in + sum(pending) (fp32); h_out = modnorm(x_out) (mode 1) or bf16(x_out) (mode 2)."""
+    lib = _lib.load()
+    _need(x_in, torch.float32, "x_in")
+    _need(x_out, torch.float32, "x_out")
+    D = x_in.shape[-1]
+    rows = x_in.numel() // D
+    if x_out.shape != x_in.shape or not x_in.is_contiguous() or not x_out.is_contiguous():
+        raise ShapeError("residual stream buffers must be contiguous and equally shaped")
+    for p in pending:
+        _need(p, torch.bfloat16, "pending term")
+        if p.numel() != x_in.numel() or not p.is_contiguous():
+            raise ShapeError(f"pending term {tuple(p.shape)} does not match residual {tuple(x_in.shape)}")
+    if h_out is not None:
+        _need(h_out, torch.bfloat16, "h_out")
+        if h_out.numel() != x_in.numel():
+            raise ShapeError("h_out does not match the residual stream")
+    pend = list(pending)
+    src = x_in
+    # more than MAX_PENDING terms: drain in order, normalising only on the last chunk
+    while len(pend) > MAX_PENDING:
+        chunk, pend = pend[:MAX_PENDING], pend[MAX_PENDING:]
+        arr = _lib.ptr_array([p.data_ptr() for p in chunk])
+        _lib.check(
+            lib.pab_residual_modnorm(src.data_ptr(), x_out.data_ptr(), arr, len(chunk), None, None, None, None,
+                                     rows, D, eps, 0, _stream()),
+            "pab_residual_modnorm",
+        )
+        src = x_out
+    arr = _lib.ptr_array([p.data_ptr() for p in pend])
+    _lib.check(
+        lib.pab_residual_modnorm(
+            src.data_ptr(), x_out.data_ptr(), arr, len(pend),
+            gamma.data_ptr() if gamma is not None else None,
+            beta.data_ptr() if beta is not None else None,
+            mod.data_ptr() if mod is not None else None,
+            h_out.data_ptr() if h_out is not None else None,
+            rows, D, float(eps), int(mode), _stream(),
+        ),
+        "pab_residual_modnorm",
+    )
+
+
+def ddim_cfg(z, r, pending, guidance: bool, guidance_scale: float, a_cur: float, a_next: float):
+    lib = _lib.load()
+    _need(z, torch.float32, "z")
+    _need(r, torch.float32, "r")
+    batch = z.shape[0]
+    n = z.numel() // batch
+    pend = list(pending)
+    while len(pend) > MAX_PENDING:  # fold excess terms into r first (same add order)
+        residual_modnorm(r, r, pend[:MAX_PENDING], mode=0)
+        pend = pend[MAX_PENDING:]
+    arr = _lib.ptr_array([p.data_ptr() for p in pend])
+    _lib.check(
+        lib.pab_ddim_cfg(z.data_ptr(), r.data_ptr(), arr, len(pend), batch, n, int(bool(guidance)),
+                         float(guidance_scale), float(a_cur), float(a_next), _stream()),
+        "pab_ddim_cfg",
+    )
+
+
+def gelu_(x: torch.Tensor) -> torch.Tensor:
+    lib = _lib.load()
+    _need(x, torch.bfloat16, "gelu input")
+    _lib.check(lib.pab_gelu_bf16(x.data_ptr(), x.data_ptr(), x.numel(), _stream()), "pab_gelu_bf16")
+    return x
+
+
+def fill_uniform(dst: torch.Tensor, rows: int, cols: int, col0: int, state: int, first_draw: int, lo: float,
+                 hi: float):
+    """Fill dst[:, col0:col0+cols] (row-major, ld = dst.shape[-1]) from a splitmix64 stream."""
+    lib = _lib.load()
+    if dst.dtype not in (torch.float32, torch.bfloat16) or not dst.is_cuda or not dst.is_contiguous():
+        raise ValidationError("fill_uniform target must be a contiguous CUDA fp32/bf16 tensor")
+    ld = dst.shape[-1]
+    dtype = 0 if dst.dtype == torch.float32 else 1
+    _lib.check(
+        lib.pab_fill_uniform(dst.data_ptr(), dtype, rows, cols, ld, col0, ctypes.c_uint64(state),
+                             ctypes.c_uint64(first_draw), float(lo), float(hi), _stream()),
+        "pab_fill_uniform",
+    )
+
+
+def attn_args(q, k, v, o, qs, ks, vs, os_, n_a, n_b, n_q, n_k, heads, dh, scale=None) -> _lib.AttnArgs:
+    """Build pab_attn_args; *s are (s_a, s_b, s_i) element strides of each operand."""
+    for t, name in ((q, "q"), (k, "k"), (v, "v"), (o, "o")):
+        _need(t, torch.bfloat16, name)
+    a = _lib.AttnArgs()
+    a.q, a.k, a.v, a.o = q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr()
+    a.q_sa, a.q_sb, a.q_si = qs
+    a.k_sa, a.k_sb, a.k_si = ks
+    a.v_sa, a.v_sb, a.v_si = vs
+    a.o_sa, a.o_sb, a.o_si = os_
+    a.n_a, a.n_b, a.n_q, a.n_k, a.heads, a.dh = n_a, n_b, n_q, n_k, heads, dh
+    a.scale = (1.0 / math.sqrt(dh)) if scale is None else scale
+    return a
+
+
+def attention(args: _lib.AttnArgs, impl: int = IMPL_AUTO) -> None:
+    lib = _lib.load()
+    _lib.check(lib.pab_attention(ctypes.byref(args), int(impl), _stream()), "pab_attention")
+
+
+def attention_select(args: _lib.AttnArgs) -> int:
+    return int(_lib.load().pab_attention_select(ctypes.byref(args)))

@@ -1,0 +1,340 @@
+"""Device-side step engine: workspaces, per-run constants and the site loop.
+
+One ``StepContext`` is built per (params, batch, text ids, timestep list):
+it owns every activation buffer of a step (fixed addresses, so attention
+argument blocks are built once), the text K/V of every cross site (step
+invariant, computed once per run), and the timestep-modulation vectors of
+every (step, layer, site) (one batched fp32 GEMM per run).
+
+``run_forward`` walks the reference's site order (model.py:505-566):
+    per layer: spatial, cross, mlp | temporal, [cross], mlp
+A computed site runs prologue -> projections -> attention/GELU -> output
+projection, writing o either into a scratch buffer or, when a later step
+reuses it, into a fresh tensor that the cache keeps.  A reused site only
+appends its cached o to the pending list.  Pending terms are added to the
+fp32 residual stream by the next prologue, in order, so arithmetic order
+matches the reference's `x = x + o` chain.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import kernels
+from .errors import PolicyError
+from .model import (
+    ATTENTION_KINDS,
+    CAT_MLP,
+    CAT_NORM_MOD,
+    CAT_OUT,
+    CAT_QKV,
+    CAT_SCORE,
+    CAT_VALUE,
+    GELU_FLOPS_PER_ELEM,
+    LN_FLOPS_PER_ELEM,
+    MOD_MLP_S,
+    MOD_MLP_T,
+    MOD_SPATIAL,
+    MOD_TEMPORAL,
+    MODULATE_FLOPS_PER_ELEM,
+    SOFTMAX_FLOPS_PER_ELEM,
+    ComponentKind,
+    ModelParams,
+    TraceRecord,
+    embed_text,
+    timestep_embedding,
+)
+
+SP, TM, CR, ML = ComponentKind.SPATIAL, ComponentKind.TEMPORAL, ComponentKind.CROSS, ComponentKind.MLP
+
+torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = False
+
+
+@dataclass
+class Launches:
+    """Per-step accounting of what ran (decision log + kernel counts)."""
+
+    sites_computed: int = 0
+    sites_reused: int = 0
+    attention_calls: int = 0
+    prologue_calls: int = 0
+    gemm_calls: int = 0
+    other_calls: int = 0
+    log: list = field(default_factory=list)  # (step, layer, kind, block, decision, source)
+
+    def own_kernels(self) -> int:
+        return self.attention_calls + self.prologue_calls + self.other_calls
+
+
+class StepContext:
+    def __init__(self):
+        pass
+
+    @classmethod
+    def build(cls, params: ModelParams, batch: int, text_ids, timesteps, frames: Optional[int] = None):
+        """frames: local frame count (sequence-parallel shards hold T/W frames)."""
+        self = cls()
+        cfg = params.cfg
+        dev = params.w_time.device
+        self.params, self.cfg, self.B = params, cfg, batch
+        self.T = cfg.frames if frames is None else frames
+        self.S, self.D, self.H = cfg.spatial_tokens, cfg.hidden, cfg.heads
+        self.dh, self.R, self.M = cfg.head_dim, cfg.mlp_hidden, cfg.text_tokens
+        self.rows = batch * self.T * self.S
+        bf = dict(device=dev, dtype=torch.bfloat16)
+        rows, D = self.rows, self.D
+        self.h = torch.empty((rows, D), **bf)
+        self.qkv = torch.empty((rows, 3 * D), **bf)
+        self.attn_out = torch.empty((rows, D), **bf)
+        self.qbuf = torch.empty((rows, D), **bf)
+        self.hidden = torch.empty((rows, self.R), **bf)
+        self.o_scratch = torch.empty((rows, D), **bf)
+        self.launches = Launches()
+        self.attn_impl = kernels.IMPL_AUTO
+
+        # per-run constants: timestep modulation for every (step, layer, slot)
+        temb = np.stack([timestep_embedding(float(t), D).astype(np.float32) for t in timesteps])
+        t_vecs = torch.as_tensor(temb, device=dev) @ params.w_time              # (N, D) fp32
+        # (L, 4, N, 2D) -> (N, L, 4, 2D)
+        self.mods = torch.matmul(t_vecs[None, None], params.w_mod_all).permute(2, 0, 1, 3).contiguous()
+
+        # per-run constants: text K/V of every cross site (step invariant)
+        emb = embed_text(params, text_ids, batch).to(torch.bfloat16).reshape(batch * self.M, D)
+        self.text_kv = []
+        for lp in params.layers:
+            kv_s = emb @ lp.cross_spatial.w_kv
+            kv_t = emb @ lp.cross_temporal.w_kv if lp.cross_temporal is not None else None
+            self.text_kv.append((kv_s, kv_t))
+
+        self._build_attention_args()
+        return self
+
+    def _build_attention_args(self):
+        B, T, S, D, H, dh, M = self.B, self.T, self.S, self.D, self.H, self.dh, self.M
+        q, k, v = self.qkv[:, :D], self.qkv[:, D : 2 * D], self.qkv[:, 2 * D :]
+        ld = 3 * D
+        # spatial: problem a = frame (B*T), rows = tokens
+        self.args_spatial = kernels.attn_args(
+            q, k, v, self.attn_out, (S * ld, 0, ld), (S * ld, 0, ld), (S * ld, 0, ld), (S * D, 0, D),
+            B * T, 1, S, S, H, dh)
+        # temporal: problem (a = batch, b = token), rows = frames (stride S rows)
+        self.args_temporal = kernels.attn_args(
+            q, k, v, self.attn_out, (T * S * ld, ld, S * ld), (T * S * ld, ld, S * ld), (T * S * ld, ld, S * ld),
+            (T * S * D, D, S * D), B, S, T, T, H, dh)
+        # cross: q rows = all (frame, token) of a batch entry, keys = text tokens
+        self.args_cross = []
+        for kv_s, kv_t in self.text_kv:
+            per = []
+            for kv in (kv_s, kv_t):
+                if kv is None:
+                    per.append(None)
+                    continue
+                kk, vv = kv[:, :D], kv[:, D:]
+                per.append(kernels.attn_args(
+                    self.qbuf, kk, vv, self.attn_out, (T * S * D, 0, D), (M * 2 * D, 0, 2 * D),
+                    (M * 2 * D, 0, 2 * D), (T * S * D, 0, D), B, 1, T * S, M, H, dh))
+            self.args_cross.append(per)
+
+
+class _Sink:
+    """Analytic flop accounting in the reference's categories (model.py:300-314)."""
+
+    def __init__(self, sink, ctx: StepContext):
+        self.sink, self.ctx = sink, ctx
+
+    def site(self, kind, block):
+        if self.sink is None:
+            return
+        c = self.ctx
+        E = c.rows * c.D
+        D, H, dh = c.D, c.H, c.dh
+        add = lambda cat, n: self.sink.add(kind, cat, int(n))  # noqa: E731
+        if kind == CR:
+            add(CAT_QKV, 2 * E * D + 2 * 2 * (c.B * c.M) * D * D)
+            score = c.B * H * c.T * c.S * c.M
+            add(CAT_SCORE, 2 * score * dh + SOFTMAX_FLOPS_PER_ELEM * score)
+            add(CAT_VALUE, 2 * c.B * H * c.T * c.S * dh * c.M)
+            add(CAT_OUT, 2 * E * D)
+            return
+        add(CAT_NORM_MOD, LN_FLOPS_PER_ELEM * E + 2 * D * 2 * D + MODULATE_FLOPS_PER_ELEM * E)
+        if kind == ML:
+            add(CAT_MLP, 2 * c.rows * D * c.R + GELU_FLOPS_PER_ELEM * c.rows * c.R + 2 * c.rows * c.R * D)
+            return
+        n = c.S if kind == SP else c.T
+        add(CAT_QKV, 3 * 2 * E * D)
+        score = c.rows * H * n
+        add(CAT_SCORE, 2 * score * dh + SOFTMAX_FLOPS_PER_ELEM * score)
+        add(CAT_VALUE, 2 * c.rows * H * dh * n)
+        add(CAT_OUT, 2 * E * D)
+
+
+class _Step:
+    """Mutable state of one forward pass."""
+
+    def __init__(self, ctx, step, t, z, r, decisions, cache, trace, flop_sink):
+        self.ctx, self.step, self.t = ctx, step, t
+        self.src, self.r = z, r
+        self.decisions, self.cache, self.trace = decisions, cache, trace
+        self.pending: list = []
+        self.sink = _Sink(flop_sink, ctx)
+        self.mods = ctx.mods[step]
+
+    # -- helpers ---------------------------------------------------------
+    def prologue(self, mode: int, mod=None, ln=None):
+        c = self.ctx
+        gamma = beta = None
+        if ln is not None and not c.params.ln_identity:
+            gamma, beta = ln
+        kernels.residual_modnorm(self.src.view(-1, c.D), self.r.view(-1, c.D), self.pending, h_out=c.h,
+                                 mod=mod, gamma=gamma, beta=beta, mode=mode)
+        c.launches.prologue_calls += 1
+        self.src = self.r
+        self.pending = []
+
+    def flush(self):
+        """Materialise the residual stream (no normalised output)."""
+        c = self.ctx
+        if self.pending or self.src is not self.r:
+            kernels.residual_modnorm(self.src.view(-1, c.D), self.r.view(-1, c.D), self.pending, mode=0)
+            c.launches.prologue_calls += 1
+        self.src = self.r
+        self.pending = []
+
+    def out_buffer(self, store: bool):
+        c = self.ctx
+        return torch.empty((c.rows, c.D), device=c.h.device, dtype=torch.bfloat16) if store else c.o_scratch
+
+    def record(self, li, kind, block, decision, source, o):
+        c = self.ctx
+        c.launches.log.append((self.step, li, kind.value, block, decision, source))
+        if self.trace is not None:
+            self.trace.observe(TraceRecord(step=self.step, timestep=self.t, layer=li, kind=kind, block=block,
+                                           decision=decision, source_step=source), o)
+
+    def run_site(self, li, kind, block, compute):
+        d = self.decisions
+        source = d.source(li, kind)
+        site = (li, kind, block)
+        c = self.ctx
+        if source == self.step:
+            store = d.should_store(li, kind)
+            o = compute(self.out_buffer(store))
+            if store:
+                self.cache.store(site, o, self.step, "outputs")
+            self.sink.site(kind, block)
+            c.launches.sites_computed += 1
+            decision = "compute"
+        else:
+            entry = self.cache.fetch(site, "outputs")
+            if entry.source_step != source:
+                raise PolicyError(f"cache for {site} holds step {entry.source_step}, table expects {source}")
+            o = entry.value
+            c.launches.sites_reused += 1
+            decision = "reuse"
+        self.pending.append(o)
+        self.record(li, kind, block, decision, source, o)
+
+    # -- site bodies -------------------------------------------------------
+    def attn_site(self, p, slot, temporal):
+        c = self.ctx
+
+        def compute(o):
+            self.prologue(1, self.mods[self._li, slot], (p.ln_gamma, p.ln_beta))
+            torch.mm(c.h, p.w_qkv, out=c.qkv)
+            kernels.attention(c.args_temporal if temporal else c.args_spatial, c.attn_impl)
+            torch.mm(c.attn_out, p.wo, out=o)
+            c.launches.attention_calls += 1
+            c.launches.gemm_calls += 2
+            return o
+
+        return compute
+
+    def cross_site(self, p, blk):
+        c = self.ctx
+
+        def compute(o):
+            self.prologue(2)
+            torch.mm(c.h, p.wq, out=c.qbuf)
+            kernels.attention(c.args_cross[self._li][blk], c.attn_impl)
+            torch.mm(c.attn_out, p.wo, out=o)
+            c.launches.attention_calls += 1
+            c.launches.gemm_calls += 2
+            return o
+
+        return compute
+
+    def mlp_site(self, p, slot):
+        c = self.ctx
+
+        def compute(o):
+            self.prologue(1, self.mods[self._li, slot], (p.ln_gamma, p.ln_beta))
+            torch.mm(c.h, p.w1, out=c.hidden)
+            kernels.gelu_(c.hidden)
+            torch.mm(c.hidden, p.w2, out=o)
+            c.launches.other_calls += 1
+            c.launches.gemm_calls += 2
+            return o
+
+        return compute
+
+    def layer(self, li, lp, temporal_hook=None):
+        self._li = li
+        d = self.decisions
+        delta = bool(getattr(d, "delta_mode", False))
+        if delta and d.layer_fully_reused(li):
+            source = d.source(li, SP)
+            entry = self.cache.fetch((li, None, "delta"), "delta")
+            if entry.source_step != source:
+                raise PolicyError(f"delta cache for layer {li} holds step {entry.source_step}, table expects {source}")
+            self.pending.append(entry.value)
+            sites = [(SP, "s"), (CR, "s"), (ML, "s"), (TM, "t"), (ML, "t")]
+            if self.ctx.cfg.cross_in_temporal:
+                sites.insert(4, (CR, "t"))
+            for kind, block in sites:
+                self.record(li, kind, block, "delta", d.source(li, kind), None)
+            return
+        x_in = None
+        if delta:
+            self.flush()
+            x_in = self.r.clone()
+        self.run_site(li, SP, "s", self.attn_site(lp.spatial, MOD_SPATIAL, False))
+        self.run_site(li, CR, "s", self.cross_site(lp.cross_spatial, 0))
+        self.run_site(li, ML, "s", self.mlp_site(lp.mlp_spatial, MOD_MLP_S))
+        if temporal_hook is not None:
+            temporal_hook(self, li, lp)
+        else:
+            self.run_site(li, TM, "t", self.attn_site(lp.temporal, MOD_TEMPORAL, True))
+        if self.ctx.cfg.cross_in_temporal:
+            self.run_site(li, CR, "t", self.cross_site(lp.cross_temporal, 1))
+        self.run_site(li, ML, "t", self.mlp_site(lp.mlp_temporal, MOD_MLP_T))
+        if x_in is not None and d.should_store_delta(li):
+            self.flush()
+            self.cache.store((li, None, "delta"), (self.r - x_in).to(torch.bfloat16), self.step, "delta")
+
+
+def run_forward(ctx: StepContext, step_index: int, t: float, z, r, decisions, cache, trace=None, flop_sink=None,
+                finish="residual", ddim=None, temporal_hook=None):
+    """Run every layer of one step.  finish="residual": r <- eps.
+    finish="ddim": z <- DDIM(z, CFG(eps)) with ddim=(guidance, g, a_cur, a_next)."""
+    st = _Step(ctx, step_index, t, z, r, decisions, cache, trace, flop_sink)
+    st.step = decisions.step
+    t0 = time.perf_counter()
+    for li, lp in enumerate(ctx.params.layers):
+        st.layer(li, lp, temporal_hook)
+    if finish == "residual":
+        st.flush()
+    else:
+        guidance, g, a_cur, a_next = ddim
+        if st.src is not st.r:  # nothing ran (L == 0 cannot happen, but stay exact)
+            st.flush()
+        kernels.ddim_cfg(z, st.r, st.pending, guidance, g, a_cur, a_next)
+        ctx.launches.other_calls += 1
+    return time.perf_counter() - t0
+
+
+__all__ = ["StepContext", "run_forward", "Launches", "ATTENTION_KINDS"]

@@ -1,0 +1,191 @@
+"""Op-level numerics of every CUDA kernel against a plain PyTorch fp32
+reference of the same op (attention, modnorm, GELU) or an exact numpy
+restatement (DDIM/CFG, splitmix fill).  Runs on the B200 only."""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2408_12588_b200 import kernels  # noqa: E402
+from paper_2408_12588_b200.numerics import RandomStream  # noqa: E402
+
+DEV = "cuda"
+
+
+def ref_attention(q, k, v):
+    """fp32 softmax(q k^T / sqrt(dh)) v on (..., n, dh) tensors."""
+    q, k, v = q.float(), k.float(), v.float()
+    s = (q @ k.transpose(-1, -2)) / math.sqrt(q.shape[-1])
+    return torch.softmax(s, dim=-1) @ v
+
+
+def check_close(got, want, tag, rel_tol=1.2e-2):
+    got, want = got.float(), want.float()
+    err = (got - want).norm() / want.norm().clamp_min(1e-12)
+    mx = (got - want).abs().max() / want.abs().max().clamp_min(1e-12)
+    assert torch.isfinite(got).all(), tag
+    assert err < rel_tol and mx < 4 * rel_tol, (tag, float(err), float(mx))
+
+
+def spatial_case(B, T, S, H, dh, impl, seed=0):
+    g = torch.Generator(device=DEV).manual_seed(seed)
+    D = H * dh
+    qkv = torch.randn(B * T * S, 3 * D, device=DEV, generator=g).to(torch.bfloat16)
+    out = torch.full((B * T * S, D), float("nan"), device=DEV, dtype=torch.bfloat16)
+    ld = 3 * D
+    a = kernels.attn_args(qkv[:, :D], qkv[:, D:2 * D], qkv[:, 2 * D:], out, (S * ld, 0, ld), (S * ld, 0, ld),
+                          (S * ld, 0, ld), (S * D, 0, D), B * T, 1, S, S, H, dh)
+    kernels.attention(a, impl)
+    torch.cuda.synchronize()
+    x = qkv.view(B * T, S, 3, H, dh).permute(2, 0, 3, 1, 4)  # (3, BT, H, S, dh)
+    want = ref_attention(x[0], x[1], x[2]).permute(0, 2, 1, 3).reshape(B * T * S, D)
+    return out, want, a
+
+
+def temporal_case(B, T, S, H, dh, impl, seed=1):
+    g = torch.Generator(device=DEV).manual_seed(seed)
+    D = H * dh
+    qkv = torch.randn(B * T * S, 3 * D, device=DEV, generator=g).to(torch.bfloat16)
+    out = torch.full((B * T * S, D), float("nan"), device=DEV, dtype=torch.bfloat16)
+    ld = 3 * D
+    st = (T * S * ld, ld, S * ld)
+    a = kernels.attn_args(qkv[:, :D], qkv[:, D:2 * D], qkv[:, 2 * D:], out, st, st, st, (T * S * D, D, S * D),
+                          B, S, T, T, H, dh)
+    kernels.attention(a, impl)
+    torch.cuda.synchronize()
+    x = qkv.view(B, T, S, 3, H, dh).permute(3, 0, 2, 4, 1, 5)  # (3, B, S, H, T, dh)
+    want = ref_attention(x[0], x[1], x[2]).permute(0, 3, 1, 2, 4).reshape(B * T * S, D)
+    return out, want, a
+
+
+def cross_case(B, N, M, H, dh, impl, seed=2):
+    g = torch.Generator(device=DEV).manual_seed(seed)
+    D = H * dh
+    q = torch.randn(B * N, D, device=DEV, generator=g).to(torch.bfloat16)
+    kv = torch.randn(B * M, 2 * D, device=DEV, generator=g).to(torch.bfloat16)
+    out = torch.full((B * N, D), float("nan"), device=DEV, dtype=torch.bfloat16)
+    a = kernels.attn_args(q, kv[:, :D], kv[:, D:], out, (N * D, 0, D), (M * 2 * D, 0, 2 * D),
+                          (M * 2 * D, 0, 2 * D), (N * D, 0, D), B, 1, N, M, H, dh)
+    kernels.attention(a, impl)
+    torch.cuda.synchronize()
+    qh = q.view(B, N, H, dh).transpose(1, 2)
+    kvh = kv.view(B, M, 2, H, dh).permute(2, 0, 3, 1, 4)
+    want = ref_attention(qh, kvh[0], kvh[1]).transpose(1, 2).reshape(B * N, D)
+    return out, want, a
+
+
+IMPLS = [kernels.IMPL_TCGEN05, kernels.IMPL_SIMT]
+
+
+@pytest.mark.parametrize("impl", IMPLS)
+@pytest.mark.parametrize("B,T,S,H,dh", [(1, 2, 1024, 2, 72), (1, 1, 1560, 2, 72), (2, 1, 200, 3, 72),
+                                         (1, 2, 16, 4, 8), (1, 1, 300, 2, 16), (1, 1, 129, 1, 64),
+                                         (1, 1, 77, 2, 32)])
+def test_spatial_attention(impl, B, T, S, H, dh):
+    out, want, a = spatial_case(B, T, S, H, dh, impl)
+    check_close(out, want, ("spatial", impl, B, T, S, H, dh))
+
+
+@pytest.mark.parametrize("impl", IMPLS)
+@pytest.mark.parametrize("B,T,S,H,dh", [(2, 16, 100, 2, 72), (1, 8, 64, 2, 72), (1, 32, 40, 2, 72),
+                                         (2, 4, 16, 4, 8), (1, 24, 30, 2, 16), (1, 16, 1560, 1, 72)])
+def test_temporal_attention(impl, B, T, S, H, dh):
+    out, want, a = temporal_case(B, T, S, H, dh, impl)
+    check_close(out, want, ("temporal", impl, B, T, S, H, dh))
+
+
+@pytest.mark.parametrize("impl", IMPLS)
+@pytest.mark.parametrize("B,N,M,H,dh", [(2, 2048, 300, 2, 72), (2, 1000, 120, 2, 72), (1, 64, 16, 2, 72),
+                                         (2, 64, 8, 4, 8), (1, 500, 5, 2, 16)])
+def test_cross_attention(impl, B, N, M, H, dh):
+    out, want, a = cross_case(B, N, M, H, dh, impl)
+    check_close(out, want, ("cross", impl, B, N, M, H, dh))
+
+
+def test_model_shapes_select_tcgen05():
+    _, _, a = spatial_case(1, 1, 256, 2, 72, kernels.IMPL_AUTO)
+    assert kernels.attention_select(a) == kernels.IMPL_TCGEN05
+    _, _, a = temporal_case(1, 16, 32, 2, 72, kernels.IMPL_AUTO)
+    assert kernels.attention_select(a) == kernels.IMPL_TCGEN05
+    _, _, a = cross_case(1, 64, 300, 2, 72, kernels.IMPL_AUTO)
+    assert kernels.attention_select(a) == kernels.IMPL_TCGEN05
+
+
+def test_cfg_null_text_gives_zero_attention():
+    # CFG null half: zero text embedding -> K = V = 0 -> output exactly 0
+    B, N, M, H, dh = 1, 256, 300, 2, 72
+    D = H * dh
+    q = torch.randn(B * N, D, device=DEV).to(torch.bfloat16)
+    kv = torch.zeros(B * M, 2 * D, device=DEV, dtype=torch.bfloat16)
+    out = torch.full((B * N, D), 7.0, device=DEV, dtype=torch.bfloat16)
+    a = kernels.attn_args(q, kv[:, :D], kv[:, D:], out, (N * D, 0, D), (M * 2 * D, 0, 2 * D),
+                          (M * 2 * D, 0, 2 * D), (N * D, 0, D), B, 1, N, M, H, dh)
+    kernels.attention(a, kernels.IMPL_TCGEN05)
+    assert torch.count_nonzero(out) == 0
+
+
+@pytest.mark.parametrize("D,n_pending,mode", [(1152, 0, 1), (1152, 2, 1), (144, 1, 2), (30, 3, 1), (64, 9, 1),
+                                              (144, 2, 0)])
+def test_residual_modnorm(D, n_pending, mode):
+    rows = 333
+    x = torch.randn(rows, D, device=DEV)
+    pend = [torch.randn(rows, D, device=DEV).to(torch.bfloat16) for _ in range(n_pending)]
+    mod = torch.randn(2 * D, device=DEV) * 0.1
+    x_out = torch.empty_like(x)
+    h = torch.empty(rows, D, device=DEV, dtype=torch.bfloat16)
+    kernels.residual_modnorm(x, x_out, pend, h_out=h if mode else None, mod=mod, mode=mode)
+    want_x = x.clone()
+    for p in pend:
+        want_x = want_x + p.float()
+    assert torch.equal(x_out, want_x)  # same fp32 add order
+    if mode == 1:
+        ln = torch.nn.functional.layer_norm(want_x, (D,), eps=1e-5)
+        want_h = ln * (1.0 + mod[D:]) + mod[:D]
+        check_close(h, want_h, "modnorm", 6e-3)
+    elif mode == 2:
+        assert torch.equal(h, want_x.to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("guidance", [False, True])
+def test_ddim_cfg_exact(guidance):
+    B = 2 if guidance else 1
+    n = 4097
+    z = torch.randn(B, n, device=DEV)
+    r = torch.randn(B, n, device=DEV)
+    pend = [torch.randn(B, n, device=DEV).to(torch.bfloat16) for _ in range(2)]
+    a_cur, a_next, g = 0.31, 0.47, 4.0
+    zn = z.cpu().numpy().copy()
+    eps = r.cpu().numpy().copy()
+    for p in pend:
+        eps = eps + p.float().cpu().numpy()
+    kernels.ddim_cfg(z, r, pend, guidance, g, a_cur, a_next)
+    if guidance:
+        e = eps[1:2] + np.float32(g) * (eps[0:1] - eps[1:2])
+        eps = np.concatenate([e, e])
+    x0 = (zn - np.float32(math.sqrt(1 - a_cur)) * eps) / np.float32(math.sqrt(a_cur))
+    want = np.float32(math.sqrt(a_next)) * x0 + np.float32(math.sqrt(1 - a_next)) * eps
+    assert np.array_equal(z.cpu().numpy(), want.astype(np.float32))
+
+
+def test_gelu():
+    x = (torch.randn(1 << 20, device=DEV) * 3).to(torch.bfloat16)
+    want = torch.nn.functional.gelu(x.float(), approximate="tanh")
+    got = kernels.gelu_(x.clone())
+    check_close(got, want, "gelu", 5e-3)
+
+
+def test_fill_uniform_matches_host_stream():
+    seed, rows, cols = 12345, 37, 53
+    host = RandomStream(seed)
+    host.uniform(1000, -0.3, 0.3)  # advance: the device fill starts at draw 1000
+    want = host.uniform(rows * cols, -0.25, 0.25).reshape(rows, cols).astype(np.float32)
+    dst = torch.zeros(rows, cols + 7, device=DEV)
+    kernels.fill_uniform(dst, rows, cols, 7, seed, 1000, -0.25, 0.25)
+    assert np.array_equal(dst[:, 7:].cpu().numpy(), want)
+    dst16 = torch.zeros(rows, cols, device=DEV, dtype=torch.bfloat16)
+    kernels.fill_uniform(dst16, rows, cols, 0, seed, 1000, -0.25, 0.25)
+    assert torch.equal(dst16, torch.from_numpy(want).to(DEV).to(torch.bfloat16))

@@ -1,0 +1,84 @@
+"""Pin the CPU oracle (oracle/pab_oracle.py) to the reference before trusting
+it: PRNG vectors and per-step latents / decision logs of reference runs
+(fixtures made by tests/golden/make_golden.py from /root/reference).  CPU only.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import pab_oracle as orc
+from paper_2408_12588_b200.numerics import RandomStream
+
+
+@pytest.fixture(scope="module")
+def prng(golden_dir):
+    return np.load(os.path.join(golden_dir, "prng.npz"))
+
+
+@pytest.mark.parametrize("seed", [0, 11, 2024, 2**63 + 5])
+def test_prng_vectors(prng, seed):
+    for stream in (orc.Stream(seed), RandomStream(seed)):
+        assert np.array_equal(stream.uniform(257, -0.125, 0.125), prng[f"uniform_{seed}"])
+        assert np.array_equal(stream.normal(301), prng[f"normal_{seed}"])
+    s = RandomStream(seed)
+    s.uniform(257, -0.125, 0.125)
+    s.normal(301)
+    assert [s.next_u64() for _ in range(5)] == [int(v) for v in prng[f"u64_{seed}"]]
+
+
+@pytest.fixture(scope="module")
+def small(golden_dir):
+    return (np.load(os.path.join(golden_dir, "small_runs.npz")),
+            json.load(open(os.path.join(golden_dir, "small_runs.json"))))
+
+
+KIND_NAMES = ("spatial", "temporal", "cross", "mlp")
+
+
+def _cfg(meta):
+    return orc.Cfg(meta["layers"], meta["hidden"], meta["heads"], meta["frames"], meta["spatial_tokens"],
+                   meta["text_tokens"], cross_in_temporal=meta["cross_in_temporal"])
+
+
+@pytest.mark.parametrize("case", ["small", "smallx"])
+@pytest.mark.parametrize("policy", ["none", "pab", "tgate", "deltadit"])
+@pytest.mark.parametrize("guidance", [0, 1])
+def test_oracle_matches_reference_runs(small, case, policy, guidance):
+    data, meta = small
+    key = f"{case}|{policy}|{guidance}"
+    cfg = _cfg(meta[case])
+    w = orc.init_weights(cfg, seed=3)
+    table = data[key + "|table"]
+    steps, log = [], []
+    orc.sample(cfg, w, orc.linear_timesteps(8), table, seed=7, guidance=bool(guidance),
+               delta_mode=meta[key]["delta"], per_step=steps, log=log)
+    ref = data[key + "|latents"]
+    for i, (got, want) in enumerate(zip(steps, ref)):
+        rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+        assert rel < 2e-5, (key, i, rel)
+    # per-site decision log (reference TraceRecord decision/source_step)
+    if not meta[key]["delta"]:
+        ref_log = data[key + "|log"]
+        got_log = np.array([[s, l, KIND_NAMES.index(k), 0 if b == "s" else 1, 0 if d == "compute" else 1, src]
+                            for (s, l, k, b, d, src) in log], dtype=np.int32)
+        assert np.array_equal(got_log, ref_log)
+
+
+def test_oracle_c1_subsample(golden_dir):
+    path = os.path.join(golden_dir, "c1_run.npz")
+    if not os.path.exists(path):
+        pytest.skip("c1 fixture not generated")
+    g = np.load(path)
+    cfg = orc.Cfg(4, 144, 2, 8, 1024, 16)
+    w = orc.init_weights(cfg, seed=11)
+    steps = []
+    orc.sample(cfg, w, orc.linear_timesteps(10), g["table"], seed=11, per_step=steps)
+    for i, x in enumerate(steps):
+        flat = x.reshape(-1)
+        sub = flat[g["idx"]]
+        rel = np.linalg.norm(sub - g["sub"][i]) / np.linalg.norm(g["sub"][i])
+        assert rel < 1e-4, (i, rel)
+        assert abs(np.linalg.norm(flat.astype(np.float64)) / g["norms"][i] - 1.0) < 1e-5
