@@ -18,6 +18,7 @@ matches the reference's `x = x + o` chain.
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Optional
@@ -95,7 +96,9 @@ class StepContext:
         self.hidden = torch.empty((rows, self.R), **bf)
         self.o_scratch = torch.empty((rows, D), **bf)
         self.launches = Launches()
-        self.attn_impl = kernels.IMPL_AUTO
+        # debugging override (the default, "auto", selects the tcgen05 kernel for every model shape)
+        self.attn_impl = {"auto": kernels.IMPL_AUTO, "tcgen05": kernels.IMPL_TCGEN05,
+                          "simt": kernels.IMPL_SIMT}[os.environ.get("PAB_ATTN_IMPL", "auto")]
 
         # per-run constants: timestep modulation for every (step, layer, slot)
         temb = np.stack([timestep_embedding(float(t), D).astype(np.float32) for t in timesteps])

@@ -81,7 +81,7 @@ def cross_case(B, N, M, H, dh, impl, seed=2):
 IMPLS = [kernels.IMPL_TCGEN05, kernels.IMPL_SIMT]
 
 
-@pytest.mark.parametrize("impl", IMPLS)
+@pytest.mark.parametrize("impl", IMPLS, ids=["tcgen05", "simt"])
 @pytest.mark.parametrize("B,T,S,H,dh", [(1, 2, 1024, 2, 72), (1, 1, 1560, 2, 72), (2, 1, 200, 3, 72),
                                          (1, 2, 16, 4, 8), (1, 1, 300, 2, 16), (1, 1, 129, 1, 64),
                                          (1, 1, 77, 2, 32)])
@@ -90,7 +90,7 @@ def test_spatial_attention(impl, B, T, S, H, dh):
     check_close(out, want, ("spatial", impl, B, T, S, H, dh))
 
 
-@pytest.mark.parametrize("impl", IMPLS)
+@pytest.mark.parametrize("impl", IMPLS, ids=["tcgen05", "simt"])
 @pytest.mark.parametrize("B,T,S,H,dh", [(2, 16, 100, 2, 72), (1, 8, 64, 2, 72), (1, 32, 40, 2, 72),
                                          (2, 4, 16, 4, 8), (1, 24, 30, 2, 16), (1, 16, 1560, 1, 72)])
 def test_temporal_attention(impl, B, T, S, H, dh):
@@ -98,7 +98,7 @@ def test_temporal_attention(impl, B, T, S, H, dh):
     check_close(out, want, ("temporal", impl, B, T, S, H, dh))
 
 
-@pytest.mark.parametrize("impl", IMPLS)
+@pytest.mark.parametrize("impl", IMPLS, ids=["tcgen05", "simt"])
 @pytest.mark.parametrize("B,N,M,H,dh", [(2, 2048, 300, 2, 72), (2, 1000, 120, 2, 72), (1, 64, 16, 2, 72),
                                          (2, 64, 8, 4, 8), (1, 500, 5, 2, 16)])
 def test_cross_attention(impl, B, N, M, H, dh):
