@@ -57,6 +57,22 @@ int pab_residual_modnorm(const float* x_in, float* x_out,
                          int64_t rows, int D, float eps, int mode, void* stream);
 
 /*
+ * Sequence-parallel variant of pab_residual_modnorm (mode 1 or 2): the input
+ * is this rank's frame shard, rows ordered (b < n_b, t < n_t, s < n_s); x_out
+ * keeps that order but h row (b, t, s) is written at send-order position
+ *   ((s / (n_s/n_w)) * n_t + t) * n_b + b) * (n_s/n_w) + s % (n_s/n_w)
+ * i.e. grouped by destination rank, so the frames->tokens all-to-all of the
+ * temporal site (reference parallel.reshard, pkg/src/pab_engine/parallel.py:
+ * 140-180, 324-326) sends h with no pack pass.  n_s % n_w == 0.
+ */
+int pab_residual_modnorm_sp(const float* x_in, float* x_out,
+                            const void* const* pending, int n_pending,
+                            const float* gamma, const float* beta,
+                            const float* mod, void* h_out,
+                            int64_t n_b, int64_t n_t, int64_t n_s, int64_t n_w,
+                            int D, float eps, int mode, void* stream);
+
+/*
  * Fused end-of-step residual drain + classifier-free guidance + DDIM (K8).
  * Replaces: the eps combine and ddim_update of diffusion.sample
  * (pkg/src/pab_engine/diffusion.py:183-189, 100-103).

@@ -50,16 +50,31 @@ struct VecT<1> {
     __device__ static void store_bf16(__nv_bfloat16* p, const float* v) { *p = __float2bfloat16_rn(v[0]); }
 };
 
+// Optional row permutation of the h output: rows (b, t, s) of a frame-sharded
+// (n_b, n_t, n_s) block are written in all-to-all send order
+// (dest = s / (n_s / n_w), t, b, s % (n_s / n_w)) so the sequence-parallel
+// frames->tokens exchange needs no pack pass.  n_w == 0: identity.
+struct RowPerm {
+    int64_t n_b, n_t, n_s, n_w;
+    __device__ __forceinline__ int64_t map(int64_t row) const {
+        if (n_w == 0) return row;
+        const int64_t s = row % n_s, bt = row / n_s, t = bt % n_t, b = bt / n_t;
+        const int64_t sw = n_s / n_w, dst = s / sw, sl = s - dst * sw;
+        return ((dst * n_t + t) * n_b + b) * sw + sl;
+    }
+};
+
 template <int VEC, int NV>
 __global__ void __launch_bounds__(256) residual_modnorm_kernel(
     const float* __restrict__ x_in, float* __restrict__ x_out, PendingList pend,
     const float* __restrict__ gamma, const float* __restrict__ beta,
     const float* __restrict__ mod, __nv_bfloat16* __restrict__ h_out,
-    int64_t rows, int D, float eps, int mode, int write_x) {
+    int64_t rows, int D, float eps, int mode, int write_x, RowPerm perm) {
     const int lane = threadIdx.x & 31;
     const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (row >= rows) return;
     const int64_t base = row * (int64_t)D;
+    const int64_t hbase = perm.map(row) * (int64_t)D;
     float v[NV][VEC];
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
@@ -77,7 +92,7 @@ __global__ void __launch_bounds__(256) residual_modnorm_kernel(
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
             const int c = (j * 32 + lane) * VEC;
-            if (c < D) VecT<VEC>::store_bf16(h_out + base + c, v[j]);
+            if (c < D) VecT<VEC>::store_bf16(h_out + hbase + c, v[j]);
         }
         return;
     }
@@ -116,7 +131,7 @@ __global__ void __launch_bounds__(256) residual_modnorm_kernel(
                 if (gamma) h = h * gamma[c + e] + beta[c + e];
                 o[e] = h * (1.0f + mod[D + c + e]) + mod[c + e];
             }
-            VecT<VEC>::store_bf16(h_out + base + c, o);
+            VecT<VEC>::store_bf16(h_out + hbase + c, o);
         }
     }
 }
@@ -125,13 +140,13 @@ template <int VEC>
 static int launch_modnorm_vec(const float* x_in, float* x_out, const PendingList& pl,
                               const float* gamma, const float* beta, const float* mod,
                               __nv_bfloat16* h, int64_t rows, int D, float eps, int mode,
-                              int write_x, cudaStream_t st) {
+                              int write_x, RowPerm perm, cudaStream_t st) {
     const int per_lane = (D + 32 * VEC - 1) / (32 * VEC);
     const int warps = 8;
     dim3 grid((unsigned)((rows + warps - 1) / warps)), block(32 * warps);
 #define PAB_MN(NVV)                                                                       \
     residual_modnorm_kernel<VEC, NVV><<<grid, block, 0, st>>>(x_in, x_out, pl, gamma, beta, \
-                                                              mod, h, rows, D, eps, mode, write_x)
+                                                              mod, h, rows, D, eps, mode, write_x, perm)
     if (per_lane <= 1) PAB_MN(1);
     else if (per_lane <= 2) PAB_MN(2);
     else if (per_lane <= 4) PAB_MN(4);
@@ -236,10 +251,33 @@ __global__ void fill_uniform_kernel(void* dst, int dtype, int64_t rows, int64_t 
 
 using namespace pab;
 
+static int residual_modnorm_impl(const float* x_in, float* x_out, const void* const* pending,
+                                 int n_pending, const float* gamma, const float* beta,
+                                 const float* mod, void* h_out, int64_t rows, int D, float eps,
+                                 int mode, RowPerm perm, void* stream);
+
 extern "C" int pab_residual_modnorm(const float* x_in, float* x_out, const void* const* pending,
                                     int n_pending, const float* gamma, const float* beta,
                                     const float* mod, void* h_out, int64_t rows, int D, float eps,
                                     int mode, void* stream) {
+    return residual_modnorm_impl(x_in, x_out, pending, n_pending, gamma, beta, mod, h_out, rows, D, eps, mode,
+                                 RowPerm{0, 0, 0, 0}, stream);
+}
+
+extern "C" int pab_residual_modnorm_sp(const float* x_in, float* x_out, const void* const* pending,
+                                       int n_pending, const float* gamma, const float* beta,
+                                       const float* mod, void* h_out, int64_t n_b, int64_t n_t,
+                                       int64_t n_s, int64_t n_w, int D, float eps, int mode, void* stream) {
+    if (n_b < 1 || n_t < 1 || n_s < 1 || n_w < 1 || n_s % n_w != 0) return PAB_ERR_SHAPE;
+    if (mode == 0) return PAB_ERR_INVALID;
+    return residual_modnorm_impl(x_in, x_out, pending, n_pending, gamma, beta, mod, h_out, n_b * n_t * n_s, D,
+                                 eps, mode, RowPerm{n_b, n_t, n_s, n_w}, stream);
+}
+
+static int residual_modnorm_impl(const float* x_in, float* x_out, const void* const* pending,
+                                 int n_pending, const float* gamma, const float* beta,
+                                 const float* mod, void* h_out, int64_t rows, int D, float eps,
+                                 int mode, RowPerm perm, void* stream) {
     if (rows < 0 || D <= 0 || n_pending < 0 || n_pending > PAB_MAX_PENDING) return PAB_ERR_SHAPE;
     if (mode < 0 || mode > 2) return PAB_ERR_INVALID;
     if (mode == 1 && mod == nullptr) return PAB_ERR_INVALID;
@@ -254,8 +292,9 @@ extern "C" int pab_residual_modnorm(const float* x_in, float* x_out, const void*
     bool aligned = (D % 4 == 0) && ((uintptr_t)x_in % 16 == 0) && ((uintptr_t)x_out % 16 == 0) &&
                    (h == nullptr || (uintptr_t)h % 8 == 0);
     for (int i = 0; i < n_pending; ++i) aligned = aligned && ((uintptr_t)pending[i] % 8 == 0);
-    if (aligned) return launch_modnorm_vec<4>(x_in, x_out, pl, gamma, beta, mod, h, rows, D, eps, mode, write_x, st);
-    return launch_modnorm_vec<1>(x_in, x_out, pl, gamma, beta, mod, h, rows, D, eps, mode, write_x, st);
+    if (aligned)
+        return launch_modnorm_vec<4>(x_in, x_out, pl, gamma, beta, mod, h, rows, D, eps, mode, write_x, perm, st);
+    return launch_modnorm_vec<1>(x_in, x_out, pl, gamma, beta, mod, h, rows, D, eps, mode, write_x, perm, st);
 }
 
 extern "C" int pab_ddim_cfg(float* z, const float* r, const void* const* pending, int n_pending,

@@ -73,6 +73,39 @@ def residual_modnorm(x_in, x_out, pending, h_out=None, mod=None, gamma=None, bet
     )
 
 
+def residual_modnorm_sp(x_in, x_out, pending, h_out, shard_shape, n_w, mod=None, gamma=None, beta=None, mode=1,
+                        eps=1e-5):
+    """residual_modnorm whose h output is written in all-to-all send order:
+    shard rows (b, t, s) of shape (n_b, n_t, n_s) -> (dest, t, b, s_local)."""
+    lib = _lib.load()
+    n_b, n_t, n_s, D = shard_shape
+    _need(x_in, torch.float32, "x_in")
+    _need(x_out, torch.float32, "x_out")
+    _need(h_out, torch.bfloat16, "h_out")
+    if x_in.numel() != n_b * n_t * n_s * D or h_out.numel() != x_in.numel():
+        raise ShapeError("sequence-parallel prologue buffers do not match the shard shape")
+    pend = list(pending)
+    src = x_in
+    while len(pend) > MAX_PENDING:
+        residual_modnorm(src, x_out, pend[:MAX_PENDING], mode=0)
+        pend, src = pend[MAX_PENDING:], x_out
+    for p in pend:
+        _need(p, torch.bfloat16, "pending term")
+        if p.numel() != x_in.numel():
+            raise ShapeError("pending term does not match the residual shard")
+    arr = _lib.ptr_array([p.data_ptr() for p in pend])
+    _lib.check(
+        lib.pab_residual_modnorm_sp(
+            src.data_ptr(), x_out.data_ptr(), arr, len(pend),
+            gamma.data_ptr() if gamma is not None else None,
+            beta.data_ptr() if beta is not None else None,
+            mod.data_ptr() if mod is not None else None, h_out.data_ptr(),
+            n_b, n_t, n_s, n_w, D, float(eps), int(mode), _stream(),
+        ),
+        "pab_residual_modnorm_sp",
+    )
+
+
 def ddim_cfg(z, r, pending, guidance: bool, guidance_scale: float, a_cur: float, a_next: float):
     lib = _lib.load()
     _need(z, torch.float32, "z")

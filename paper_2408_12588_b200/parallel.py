@@ -1,0 +1,462 @@
+"""Broadcast sequence parallelism over real GPUs (one process per GPU).
+
+Drop-in for pkg/src/pab_engine/parallel.py.  The reference runs W *logical*
+workers sequentially in one process (parallel.py:1-15); here each worker is
+a rank of a torch.distributed NCCL group on its own B200:
+
+* the residual stream is frame-sharded: rank w owns frames
+  [w T/W, (w+1) T/W) of every batch entry, (B, T/W, S, D) fp32;
+* spatial, cross and MLP sites are frame/token local and run unchanged on
+  the shard (same kernels as the serial path);
+* a temporal site that COMPUTES runs the dimension switch of reference
+  `_parallel_forward_step` (parallel.py:322-340): the modulated-norm
+  prologue writes bf16 h straight into all-to-all send order (dest rank, t,
+  b, s) -> NCCL all-to-all frames->tokens -> QKV GEMM, temporal attention
+  over all T frames for S/W tokens, output GEMM -> all-to-all tokens->frames
+  -> unpack to the frame shard.  LN is row-wise, so normalising before the
+  exchange equals the reference's reshard-then-normalise;
+* a temporal site that is BROADCAST appends this rank's cached frame-layout
+  output and launches no collective at all (parallel.py:341-348).
+
+The communication ledger records one entry per reshard with the reference's
+element count B*T*S*D*(W-1)/W (parallel.py:130-133, 167-179), so the
+executed event count equals 2 * L * |temporal compute steps|.
+"""
+
+from __future__ import annotations
+
+import csv
+from collections import defaultdict
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from .diffusion import DEFAULT_NOISE, NoiseParams, default_text_ids, initial_latent
+from .errors import PolicyError, ShapeError, ValidationError
+from .model import ComponentKind, ModelParams
+from .policies import CacheStore, DecisionTable, PabPolicy, PolicyConfig, build_schedule
+
+METHOD_COSTS = {"megatron_sp": 16, "ds_ulysses": 4, "dsp": 2, "broadcast_sp": 2}
+EXECUTABLE_METHODS = ("dsp", "broadcast_sp")
+TM = ComponentKind.TEMPORAL
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    workers: int
+    frames: int
+    spatial_tokens: int
+
+    @property
+    def frames_per_worker(self) -> int:
+        return self.frames // self.workers
+
+    @property
+    def tokens_per_worker(self) -> int:
+        return self.spatial_tokens // self.workers
+
+
+def plan_shards(workers: int, cfg) -> ShardPlan:
+    """W must divide both T and S; no padding (reference parallel.py:72-80)."""
+    if workers < 1:
+        raise ValidationError(f"worker count must be >= 1, got {workers}")
+    if cfg.frames % workers or cfg.spatial_tokens % workers:
+        raise ValidationError(
+            f"{workers} workers must divide frames ({cfg.frames}) and spatial tokens ({cfg.spatial_tokens});"
+            " padding is unsupported"
+        )
+    return ShardPlan(workers=workers, frames=cfg.frames, spatial_tokens=cfg.spatial_tokens)
+
+
+@dataclass
+class CommEntry:
+    step: int
+    layer: int
+    method: str
+    elements: int
+    bytes: int
+    communicating: bool
+    wire_bytes: int = 0  # bytes this rank actually sent over NVLink (bf16 payload)
+
+
+@dataclass
+class CommReport:
+    method: str
+    workers: int
+    bytes_per_element: int
+    cost_constant: int = 0
+    entries: list = field(default_factory=list)
+
+    def total_elements(self) -> int:
+        return sum(e.elements for e in self.entries)
+
+    def total_bytes(self) -> int:
+        return sum(e.bytes for e in self.entries)
+
+    def grouped_elements(self) -> dict:
+        out: dict = defaultdict(int)
+        for e in self.entries:
+            if e.elements:
+                out[(e.step, e.layer)] += e.elements
+        return dict(out)
+
+    def event_count(self) -> int:
+        return sum(1 for e in self.entries if e.communicating)
+
+    def write_csv(self, path):
+        with open(path, "w", newline="") as fh:
+            w = csv.writer(fh)
+            w.writerow(["step", "layer", "method", "elements", "bytes", "communicating"])
+            for e in self.entries:
+                w.writerow([e.step, e.layer, e.method, e.elements, e.bytes, int(e.communicating)])
+
+
+def _alltoall_elements(batch: int, cfg, workers: int) -> int:
+    total = batch * cfg.frames * cfg.spatial_tokens * cfg.hidden
+    return total // workers * (workers - 1)
+
+
+_AXIS = {"frames": 1, "tokens": 2}
+
+
+def split_shards(full, axis: str, workers: int) -> list:
+    """Split a (B, T, S, D) array/tensor along frames or tokens (contiguous shards)."""
+    ax = _AXIS[axis]
+    n = full.shape[ax] // workers
+    parts = [full[(slice(None),) * ax + (slice(i * n, (i + 1) * n),)] for i in range(workers)]
+    if isinstance(full, np.ndarray):
+        return [np.ascontiguousarray(p) for p in parts]
+    return [p.contiguous() for p in parts]
+
+
+def reshard(shards: Sequence, from_axis: str, to_axis: str, plan: ShardPlan, cfg, ledger: Optional[CommReport] = None,
+            step: int = -1, layer: int = -1) -> list:
+    """Value-preserving repartition of in-process shards (reference API,
+    parallel.py:140-180).  The distributed engine uses `exchange_*` below."""
+    if from_axis not in _AXIS or to_axis not in _AXIS:
+        raise ValidationError(f"unknown layout axes {from_axis!r} -> {to_axis!r}")
+    if from_axis == to_axis:
+        raise ShapeError("reshard endpoints must differ")
+    if len(shards) != plan.workers:
+        raise ShapeError(f"expected {plan.workers} shards, got {len(shards)}")
+    want = plan.frames_per_worker if from_axis == "frames" else plan.tokens_per_worker
+    for s in shards:
+        if s.shape[_AXIS[from_axis]] != want:
+            raise ShapeError(f"shard shape {tuple(s.shape)} does not match the {from_axis} layout")
+    if isinstance(shards[0], np.ndarray):
+        full = np.concatenate(shards, axis=_AXIS[from_axis])
+    else:
+        import torch
+
+        full = torch.cat(list(shards), dim=_AXIS[from_axis])
+    if ledger is not None:
+        el = _alltoall_elements(shards[0].shape[0], cfg, plan.workers)
+        ledger.entries.append(CommEntry(step, layer, ledger.method, el, el * ledger.bytes_per_element, el > 0))
+    return split_shards(full, to_axis, plan.workers)
+
+
+def comm_volume_model(method: str, cfg, schedule, table: DecisionTable, workers: int, bytes_per_element: int = 4,
+                      batch: int = 1, split_batch: bool = False) -> CommReport:
+    """Closed-form volume: c(method) * B*T*S*D*(W-1)/W per (step, layer) whose
+    temporal attention computes (reference parallel.py:183-233)."""
+    if method not in METHOD_COSTS:
+        raise ValidationError(f"unknown parallel method {method!r}")
+    ts = getattr(schedule, "timesteps", schedule)
+    if table.num_steps != len(ts):
+        raise ValidationError("table does not match the schedule")
+    rep = CommReport(method, workers, bytes_per_element, METHOD_COSTS[method])
+    groups = 2 if (split_batch and batch == 2 and workers >= 2 and workers % 2 == 0) else 1
+    gw = workers // groups
+    unit = groups * _alltoall_elements(batch // groups, cfg, gw) if gw > 1 else 0
+    comp = table.compute_mask()[:, :, 1]
+    for step in range(table.num_steps):
+        for layer in range(table.layers):
+            on = bool(comp[step, layer])
+            el = METHOD_COSTS[method] * unit if on else 0
+            rep.entries.append(CommEntry(step, layer, method, el, el * bytes_per_element, on and el > 0))
+    return rep
+
+
+# ---------------------------------------------------------------- exchange
+def send_order(h_shard, n_w: int):
+    """Reference layout transform the CUDA prologue fuses: (B, T/W, S, D) ->
+    (W, T/W, B, S/W, D) grouped by destination rank (used by tests)."""
+    B, Tl, S, D = h_shard.shape
+    return h_shard.reshape(B, Tl, n_w, S // n_w, D).permute(2, 1, 0, 3, 4).contiguous()
+
+
+def _all_to_all(recv, send, group):
+    """NCCL all-to-all on device buffers.  A gloo group (CPU tests, or several
+    ranks sharing one GPU in the single-GPU test harness) has no device
+    all-to-all, so device tensors are staged through host memory there."""
+    import torch.distributed as dist
+
+    if send.is_cuda and dist.get_backend(group) == "gloo":
+        host = recv.cpu()
+        dist.all_to_all_single(host, send.cpu(), group=group)
+        recv.copy_(host)
+        return
+    dist.all_to_all_single(recv, send, group=group)
+
+
+def _all_gather(t, group=None):
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        parts = [torch.empty_like(t, device="cpu") for _ in range(world)]
+        dist.all_gather(parts, t.cpu(), group=group)
+        return [p.to(t.device) for p in parts]
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t, group=group)
+    return parts
+
+
+def exchange_frames_to_tokens(send, recv, group=None):
+    """send: (W, T/W, B, S/W, D) by destination -> recv: (W_src, T/W, B, S/W, D)
+    = (T, B, S/W, D) token layout (frame index = src * T/W + t)."""
+    _all_to_all(recv, send, group)
+
+
+def exchange_tokens_to_frames(send, recv, group=None):
+    """send: (T, B, S/W, D) = (W_dst, T/W, B, S/W, D) -> recv: (W_src, T/W, B, S/W, D)."""
+    _all_to_all(recv, send, group)
+
+
+def unpack_frames(recv, out):
+    """(W_src, T/W, B, S/W, D) -> frame shard (B, T/W, S, D) (one bf16 pass)."""
+    W, Tl, B, Sw, D = recv.shape
+    out.view(B, Tl, W, Sw, D).copy_(recv.permute(2, 1, 0, 3, 4))
+    return out
+
+
+class _SPTemporal:
+    """Token-layout workspaces + the temporal-site hook for run_forward."""
+
+    def __init__(self, ctx, world: int, group, ledger: CommReport, bytes_per_element: int):
+        import torch
+
+        from . import kernels
+
+        self.ctx, self.W, self.group, self.ledger = ctx, world, group, ledger
+        B, Tl, S, D = ctx.B, ctx.T, ctx.S, ctx.D
+        T, Sw = Tl * world, S // world
+        self.T, self.Sw = T, Sw
+        dev = ctx.h.device
+        bf = dict(device=dev, dtype=torch.bfloat16)
+        rows_tok = T * B * Sw  # == ctx.rows
+        self.h_send = ctx.h.view(world, Tl, B, Sw, D)
+        self.h_tok = torch.empty((T, B, Sw, D), **bf)
+        self.qkv_tok = torch.empty((rows_tok, 3 * D), **bf)
+        self.attn_tok = torch.empty((rows_tok, D), **bf)
+        self.o_tok = torch.empty((T, B, Sw, D), **bf)
+        self.o_recv = torch.empty((world, Tl, B, Sw, D), **bf)
+        q, k, v = self.qkv_tok[:, :D], self.qkv_tok[:, D:2 * D], self.qkv_tok[:, 2 * D:]
+        ld = 3 * D
+        # token layout rows (t, b, s): problem (a = b, b_idx = s), rows i = t (stride B*Sw rows)
+        st = (Sw * ld, ld, B * Sw * ld)
+        self.args = kernels.attn_args(q, k, v, self.attn_tok, st, st, st, (Sw * D, D, B * Sw * D), B, Sw, T, T,
+                                      ctx.H, ctx.dh)
+        self.el = _alltoall_elements(B, ctx.cfg, world)
+        self.wire = Tl * B * Sw * D * 2 * (world - 1)
+        self.bpe = bytes_per_element
+
+    def __call__(self, st, li, lp):
+        import torch
+
+        from . import kernels
+        from .model import MOD_TEMPORAL
+
+        ctx, d = self.ctx, st.decisions
+        source = d.source(li, TM)
+        site = (li, TM, "t")
+        if source == st.step:
+            store = d.should_store(li, TM)
+            p = lp.temporal
+            kernels.residual_modnorm_sp(st.src.view(-1, ctx.D), st.r.view(-1, ctx.D), st.pending, ctx.h,
+                                        (ctx.B, ctx.T, ctx.S, ctx.D), self.W, mod=st.mods[li, MOD_TEMPORAL],
+                                        mode=1)
+            ctx.launches.prologue_calls += 1
+            st.src, st.pending = st.r, []
+            exchange_frames_to_tokens(self.h_send, self.h_tok, self.group)
+            self._log(st.step, li)
+            torch.mm(self.h_tok.view(-1, ctx.D), p.w_qkv, out=self.qkv_tok)
+            kernels.attention(self.args, ctx.attn_impl)
+            torch.mm(self.attn_tok, p.wo, out=self.o_tok.view(-1, ctx.D))
+            exchange_tokens_to_frames(self.o_tok, self.o_recv, self.group)
+            self._log(st.step, li)
+            o = st.out_buffer(store)
+            unpack_frames(self.o_recv, o.view(ctx.B, ctx.T, ctx.S, ctx.D))
+            if store:
+                st.cache.store(site, o, st.step, "outputs")
+            ctx.launches.attention_calls += 1
+            ctx.launches.gemm_calls += 2
+            ctx.launches.sites_computed += 1
+            decision = "compute"
+        else:
+            entry = st.cache.fetch(site, "outputs")
+            if entry.source_step != source:
+                raise PolicyError(f"temporal cache holds step {entry.source_step}, table expects {source}")
+            o = entry.value
+            ctx.launches.sites_reused += 1
+            decision = "reuse"
+        st.pending.append(o)
+        st.record(li, TM, "t", decision, source, o)
+
+    def _log(self, step, layer):
+        self.ledger.entries.append(CommEntry(step, layer, self.ledger.method, self.el, self.el * self.bpe,
+                                             self.el > 0, self.wire))
+
+
+class ShardedDenoiser:
+    """Frame-sharded denoising run on this rank (broadcast SP)."""
+
+    def __init__(self, params: ModelParams, schedule, table: DecisionTable, text_ids, *, guidance: bool,
+                 guidance_scale: float, rank: int, world: int, group=None, method: str = "broadcast_sp",
+                 noise_params: NoiseParams = DEFAULT_NOISE, bytes_per_element: int = 4, trace=None):
+        from .runtime import StepContext
+
+        cfg = params.cfg
+        self.plan = plan_shards(world, cfg)
+        self.params, self.table, self.rank, self.world, self.group = params, table, rank, world, group
+        self.guidance, self.g = bool(guidance), float(guidance_scale)
+        self.batch = 2 if guidance else 1
+        ids = np.asarray(text_ids, dtype=np.int64)
+        self.ids = np.stack([ids, np.full_like(ids, -1)]) if guidance else ids[None, :]
+        ts = list(getattr(schedule, "timesteps", schedule))
+        self.timesteps = ts
+        self.alphas = [(noise_params.alpha_bar(t), noise_params.alpha_bar(ts[i + 1]) if i + 1 < len(ts) else 1.0)
+                       for i, t in enumerate(ts)]
+        self.ctx = StepContext.build(params, self.batch, self.ids, ts, frames=self.plan.frames_per_worker)
+        self.ledger = CommReport(method, world, bytes_per_element, METHOD_COSTS[method])
+        self.hook = _SPTemporal(self.ctx, world, group, self.ledger, bytes_per_element) if world > 1 else None
+        self.cache = CacheStore()
+        self.trace = trace
+        self._r = None
+
+    def shard_input(self, x_full):
+        """This rank's frames of a full (B, T, S, D) latent (contiguous copy)."""
+        n = self.plan.frames_per_worker
+        return x_full[:, self.rank * n:(self.rank + 1) * n].contiguous()
+
+    def run(self, z, on_step=None):
+        import torch
+
+        from .runtime import run_forward
+
+        if self._r is None or self._r.shape != z.shape:
+            self._r = torch.empty_like(z)
+        for i, t in enumerate(self.timesteps):
+            a_cur, a_next = self.alphas[i]
+            run_forward(self.ctx, i, t, z, self._r, self.table.slice(i), self.cache, trace=self.trace,
+                        finish="ddim", ddim=(self.guidance, self.g, a_cur, a_next), temporal_hook=self.hook)
+            if on_step is not None:
+                on_step(i, z)
+        return z
+
+    def __call__(self, x_host, out=None):
+        """Serving call on this rank: H2D of its frames of the pinned host
+        latent, denoise, D2H of its frames into `out` (or a new tensor)."""
+        n = self.plan.frames_per_worker
+        sl = slice(self.rank * n, (self.rank + 1) * n)
+        z = x_host[:, sl].to(self.params.w_time.device, non_blocking=True)
+        self.run(z)
+        if out is None:
+            return z.cpu()
+        out[:, sl].copy_(z, non_blocking=True)
+        return out
+
+
+@dataclass
+class ParallelRunResult:
+    latent: np.ndarray
+    comm_report: CommReport
+    plan: ShardPlan
+    worker_caches: list
+
+    def gathered_cache(self) -> dict:
+        """Frame-concatenated cache snapshots.  Multi-process runs only hold this
+        rank's shard, so gathering goes through all_gather (collective)."""
+        import torch
+
+        merged: dict = {}
+        if not self.worker_caches:
+            return merged
+        local = self.worker_caches[0]
+        world = self.plan.workers
+        import torch.distributed as dist
+
+        multi = dist.is_available() and dist.is_initialized() and world > 1
+        for site, entry in sorted(local.entries.items(), key=lambda kv: str(kv[0])):
+            v = entry.value
+            if multi:
+                parts = _all_gather(v.contiguous())
+            else:
+                parts = [c.entries[site].value for c in self.worker_caches]
+            B = self._batch
+            parts = [p.reshape(B, -1, *self._tail) for p in parts]
+            merged[site] = torch.cat(parts, dim=1).float().cpu().numpy()
+        return merged
+
+
+def run_parallel(
+    params: ModelParams,
+    schedule,
+    policy: PolicyConfig,
+    workers: int,
+    method: str = "dsp",
+    seed: int = 0,
+    text_ids: Optional[Sequence[int]] = None,
+    *,
+    guidance: bool = False,
+    guidance_scale: float = 4.0,
+    split_batch: bool = False,
+    range_semantics: str = "period",
+    noise_params: NoiseParams = DEFAULT_NOISE,
+    table: Optional[DecisionTable] = None,
+    bytes_per_element: int = 4,
+) -> ParallelRunResult:
+    """Sequence-parallel sampler (reference parallel.run_parallel, parallel.py:372-464).
+
+    Every rank of an initialised torch.distributed group of size ``workers``
+    calls this collectively (one process per GPU, NCCL); each returns the
+    gathered full latent.  ``workers == 1`` without a process group runs the
+    single-GPU engine.
+    """
+    import torch
+    import torch.distributed as dist
+
+    cfg = params.cfg
+    if method not in EXECUTABLE_METHODS:
+        raise ValidationError(f"method {method!r} is not executable; use comm_volume_model for it")
+    if method == "broadcast_sp" and not isinstance(policy, PabPolicy):
+        raise ValidationError("broadcast_sp requires a PAB policy")
+    if split_batch and guidance and workers >= 2 and workers % 2 == 0:
+        raise ValidationError("split_batch (CFG halves on separate rank groups) is not implemented yet")
+    if table is None:
+        table = build_schedule(policy, schedule, cfg.layers, range_semantics=range_semantics)
+    if text_ids is None:
+        text_ids = default_text_ids(params)
+    multi = dist.is_available() and dist.is_initialized()
+    world = dist.get_world_size() if multi else 1
+    rank = dist.get_rank() if multi else 0
+    if workers != world:
+        raise ValidationError(f"run_parallel(workers={workers}) must run in a process group of that size "
+                              f"(got world size {world}); launch with torchrun --nproc-per-node {workers}")
+    den = ShardedDenoiser(params, schedule, table, text_ids, guidance=guidance, guidance_scale=guidance_scale,
+                          rank=rank, world=world, method=method, noise_params=noise_params,
+                          bytes_per_element=bytes_per_element)
+    x_full = torch.from_numpy(initial_latent(params, seed, den.batch)).to(params.w_time.device)
+    z = den.shard_input(x_full)
+    den.run(z)
+    if world > 1:
+        latent = torch.cat(_all_gather(z), dim=1)
+    else:
+        latent = z
+    res = ParallelRunResult(latent=latent.cpu().numpy(), comm_report=den.ledger, plan=den.plan,
+                            worker_caches=[den.cache])
+    res._batch = den.batch
+    res._tail = (cfg.spatial_tokens, cfg.hidden)
+    return res
