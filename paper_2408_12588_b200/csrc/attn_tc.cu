@@ -3,11 +3,12 @@
 // reference op: numerics.scaled_dot_attention (pkg/src/pab_engine/numerics.py:133-151)
 // as used by the spatial, temporal and cross sites (model.py:327-385).
 //
-// CTA layout (320 threads, one CTA per SM):
-//   warps 0-3  softmax group 0  -> query tile 0 (128 rows, 1 thread = 1 row = 1 TMEM lane)
-//   warps 4-7  softmax group 1  -> query tile 1
-//   warp  8    TMA producer (one elected lane)
-//   warp  9    TMEM allocator + MMA issuer (one elected lane)
+// CTA layout (576 threads, one CTA per SM):
+//   warps 0-7   softmax for query tile 0, warps 8-15 for query tile 1; within a
+//               tile, warps w and w+4 own the same 32 rows (TMEM lanes) and the
+//               left / right 64 score columns, exchanging the row max through smem
+//   warp  16    TMA producer (one elected lane)
+//   warp  17    TMEM allocator + MMA issuer (one elected lane)
 // Per KV tile j the MMA lane issues, ping-ponging the two query tiles,
 //   S_i = Q_i K_j^T  (M=128, N=128, K=dh padded to 16)  -> TMEM cols [128 i, 128 i + 128)
 //   O_i += P_i V_j   (M=128, N=64|16 blocks, K=128)      -> TMEM cols [256 + 128 i, ...)
@@ -33,7 +34,11 @@ namespace pab {
 
 namespace tc {
 
-constexpr int kThreads = 320;
+constexpr int kSoftmaxWarps = 16;
+constexpr int kTmaWarp = 16;
+constexpr int kMmaWarp = 17;
+constexpr int kThreads = 32 * (kSoftmaxWarps + 2);
+constexpr int kGroupThreads = 256;  // softmax threads per query tile
 constexpr int kRows = 128;       // query rows per tile == TMEM lanes
 constexpr int kKv = 128;         // keys per KV tile
 constexpr int kPBytes = kRows * kKv * 2;
@@ -73,6 +78,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// producer-side wait with a nanosleep backoff so a far-ahead TMA lane does not
+// steal issue slots from the softmax warps sharing its SM sub-partition
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t done = 0;
+    while (true) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+        if (done) break;
+        __nanosleep(256);
+    }
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 b2 = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&b2);
+}
+
 __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                             int c2, int c3, int c4) {
     asm volatile(
@@ -88,16 +118,22 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
+// tcgen05.mma / commit are issued by one elected lane of a warp that runs the
+// issue loop warp-wide, so descriptors stay in uniform registers
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
 }
 __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                        uint32_t accumulate) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
+        "{\n\t.reg .pred p, e;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
@@ -169,7 +205,8 @@ struct Geometry {
     static constexpr int kK0 = 2 * kTileBytes;     // 2 K stages
     static constexpr int kV0 = 4 * kTileBytes;     // 2 V stages
     static constexpr int kP0 = 6 * kTileBytes;     // 2 P tiles
-    static constexpr int kBar = kP0 + 2 * kPBytes;
+    static constexpr int kX0 = kP0 + 2 * kPBytes;  // row max / row sum exchange: [tile][half][slot][128] f32
+    static constexpr int kBar = kX0 + 2 * 2 * 3 * kRows * 4;
     static constexpr int kSmem = kBar + 256 + 1024;  // + barriers + alignment slack
 };
 
@@ -192,27 +229,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int pair = blockIdx.x, h = blockIdx.y, az = blockIdx.z;
     // problem coordinates of the two query tiles
-    int a_idx, b_idx0, i_base[2], b_base[2];
+    // problem coordinates of the two query tiles (t = 0, 1); kept as scalar
+    // expressions so no local-memory array is indexed by a runtime t
+    int a_idx, b_idx0;
     if (p.packed) {
         a_idx = az;
         b_idx0 = 0;
-        for (int t = 0; t < 2; ++t) {
-            b_base[t] = (2 * pair + t) * p.packed;
-            i_base[t] = 0;
-        }
     } else {
         a_idx = az / p.n_b;
         b_idx0 = az - a_idx * p.n_b;
-        for (int t = 0; t < 2; ++t) {
-            b_base[t] = b_idx0;
-            i_base[t] = (2 * pair + t) * kRows;
-        }
     }
+    auto i_base = [&](int t) { return p.packed ? 0 : (2 * pair + t) * kRows; };
+    auto b_base = [&](int t) { return p.packed ? (2 * pair + t) * p.packed : b_idx0; };
     const int box_rows = p.packed ? p.packed * p.n_k : kRows;  // rows a TMA box fills
     const uint32_t box_bytes = (uint32_t)box_rows * (uint32_t)(N128 * 128 + N32 * 32);
 
     // ---------------------------------------------------------------- setup
-    if (warp == 8 && lane == 0) {
+    if (warp == kTmaWarp && lane == 0) {
         prefetch_map(&q128); prefetch_map(&k128); prefetch_map(&v128);
         if (N32) { prefetch_map(&q32); prefetch_map(&k32); prefetch_map(&v32); }
         mbar_init(&bars->q_full, 1);
@@ -221,13 +254,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&bars->v_full[s], 1);
             mbar_init(&bars->kv_empty[s], 1);
             mbar_init(&bars->s_full[s], 1);
-            mbar_init(&bars->s_free[s], kRows);
-            mbar_init(&bars->p_full[s], kRows);
+            mbar_init(&bars->s_free[s], kGroupThreads);
+            mbar_init(&bars->p_full[s], kGroupThreads);
             mbar_init(&bars->o_done[s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 9) {
+    if (warp == kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(&bars->tmem_base)),
                      "r"(kTmemCols));
@@ -247,25 +280,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = bars->tmem_base;
     const int n_kv = p.n_kv;
 
-    if (warp == 8) {
+    if (warp == kTmaWarp) {
         // ===================================================== TMA producer
         if (lane == 0) {
             mbar_expect_tx(&bars->q_full, 2 * box_bytes);
             for (int t = 0; t < 2; ++t) {
                 uint8_t* dst = smem + G::kQ0 + t * G::kTileBytes;
                 for (int blk = 0; blk < N128; ++blk)
-                    tma_load_5d(dst + blk * 16384, &q128, &bars->q_full, 64 * blk, h, i_base[t], b_base[t], a_idx);
+                    tma_load_5d(dst + blk * 16384, &q128, &bars->q_full, 64 * blk, h, i_base(t), b_base(t), a_idx);
                 for (int blk = 0; blk < N32; ++blk)
                     tma_load_5d(dst + N128 * 16384 + blk * 4096, &q32, &bars->q_full, 64 * N128 + 16 * blk, h,
-                                i_base[t], b_base[t], a_idx);
+                                i_base(t), b_base(t), a_idx);
             }
             for (int j = 0; j < n_kv; ++j) {
                 const int st = j & 1;
-                if (j >= 2) mbar_wait(&bars->kv_empty[st], ((j >> 1) - 1) & 1);
+                if (j >= 2) mbar_wait_sleep(&bars->kv_empty[st], ((j >> 1) - 1) & 1);
                 const int kv_i = p.packed ? 0 : j * kKv;
                 // packed mode: each query tile owns its sequences, so KV tile j
                 // (j < 2) holds the keys of query tile j
-                const int kv_b_eff = p.packed ? b_base[j] : b_idx0;
+                const int kv_b_eff = b_base(j);
                 uint8_t* kd = smem + G::kK0 + st * G::kTileBytes;
                 uint8_t* vd = smem + G::kV0 + st * G::kTileBytes;
                 mbar_expect_tx(&bars->kv_full[st], box_bytes);
@@ -282,9 +315,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 kv_i, kv_b_eff, a_idx);
             }
         }
-    } else if (warp == 9) {
-        // ====================================================== MMA issuer
-        if (lane == 0) {
+    } else if (warp == kMmaWarp) {
+        // ====================================================== MMA issuer (warp-wide)
+        {
             constexpr uint32_t idS = idesc_bf16(128, 128, 0);
             constexpr uint32_t idO64 = idesc_bf16(128, 64, 1);
             constexpr uint32_t idO16 = idesc_bf16(128, 16, 1);
@@ -294,37 +327,49 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t p_addr = smem_u32(smem + G::kP0);
             mbar_wait(&bars->q_full, 0);
             tc_fence_after();
+            // descriptors: constant layout bits | (address >> 4); moving the start
+            // address by `off` bytes adds off >> 4 to the low word (no carry: < 256 KB)
+            const uint64_t dq128 = smem_desc(q_addr, 16, 1024, kLayoutSW128);
+            const uint64_t dk128 = smem_desc(k_addr, 16, 1024, kLayoutSW128);
+            const uint64_t dq32 = smem_desc(q_addr + N128 * 16384, 16, 256, kLayoutSW32);
+            const uint64_t dk32 = smem_desc(k_addr + N128 * 16384, 16, 256, kLayoutSW32);
+            const uint64_t dp = smem_desc(p_addr, 16, 1024, kLayoutSW128);
+            const uint64_t dv128 = smem_desc(v_addr, 16, 1024, kLayoutSW128);
+            const uint64_t dv32 = smem_desc(v_addr + N128 * 16384, 16, 256, kLayoutSW32);
             // S_t = Q_t K^T over the dh K-blocks
             auto issue_s = [&](int t, int st) {
-                const uint32_t qa = q_addr + t * G::kTileBytes, ka = k_addr + st * G::kTileBytes;
+                const uint32_t qo = (t * G::kTileBytes) >> 4, ko = (st * G::kTileBytes) >> 4;
                 const uint32_t d = tmem + 128 * t;
                 uint32_t acc = 0;
+#pragma unroll
                 for (int blk = 0; blk < N128; ++blk)
+#pragma unroll
                     for (int k = 0; k < 4; ++k) {
-                        tc_mma(d, smem_desc(qa + blk * 16384 + 32 * k, 16, 1024, kLayoutSW128),
-                               smem_desc(ka + blk * 16384 + 32 * k, 16, 1024, kLayoutSW128), idS, acc);
+                        const uint32_t o = (blk * 16384 + 32 * k) >> 4;
+                        tc_mma(d, dq128 + qo + o, dk128 + ko + o, idS, acc);
                         acc = 1;
                     }
+#pragma unroll
                 for (int blk = 0; blk < N32; ++blk) {
-                    tc_mma(d, smem_desc(qa + N128 * 16384 + blk * 4096, 16, 256, kLayoutSW32),
-                           smem_desc(ka + N128 * 16384 + blk * 4096, 16, 256, kLayoutSW32), idS, acc);
+                    const uint32_t o = (blk * 4096) >> 4;
+                    tc_mma(d, dq32 + qo + o, dk32 + ko + o, idS, acc);
                     acc = 1;
                 }
             };
             // O_t += P_t V over 8 K-steps of 16 keys, per 64- / 16-wide dh block
             auto issue_pv = [&](int t, int st, uint32_t accumulate) {
-                const uint32_t pa = p_addr + t * kPBytes, va = v_addr + st * G::kTileBytes;
+                const uint32_t po = (t * kPBytes) >> 4, vo = (st * G::kTileBytes) >> 4;
                 const uint32_t d = tmem + 256 + 128 * t;
+#pragma unroll 2
                 for (int k = 0; k < kKv / 16; ++k) {
-                    const uint64_t a_desc = smem_desc(pa + (k >> 2) * 16384 + 32 * (k & 3), 16, 1024, kLayoutSW128);
+                    const uint64_t a_desc = dp + po + (((k >> 2) * 16384 + 32 * (k & 3)) >> 4);
                     const uint32_t acc = (accumulate || k > 0) ? 1u : 0u;
+#pragma unroll
                     for (int blk = 0; blk < N128; ++blk)
-                        tc_mma(d + 64 * blk, a_desc, smem_desc(va + blk * 16384 + 2048 * k, 16, 1024, kLayoutSW128),
-                               idO64, acc);
+                        tc_mma(d + 64 * blk, a_desc, dv128 + vo + ((blk * 16384 + 2048 * k) >> 4), idO64, acc);
+#pragma unroll
                     for (int blk = 0; blk < N32; ++blk)
-                        tc_mma(d + 64 * N128 + 16 * blk, a_desc,
-                               smem_desc(va + N128 * 16384 + blk * 4096 + 512 * k, 16, 256, kLayoutSW32), idO16,
-                               acc);
+                        tc_mma(d + 64 * N128 + 16 * blk, a_desc, dv32 + vo + ((blk * 4096 + 512 * k) >> 4), idO16, acc);
                 }
             };
             if (p.packed) {
@@ -375,129 +420,159 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ================================================= softmax groups
-        const int t = warp >> 2;            // query tile of this group
+        const int t = warp >> 3;            // query tile of this group
+        const int hc = (warp >> 2) & 1;     // score-column half: [64 hc, 64 hc + 64)
         const int wl = warp & 3;            // TMEM lane quarter
         const int row = wl * 32 + lane;     // tile row owned by this thread
         const uint32_t lane_off = (uint32_t)(wl * 32) << 16;
-        const uint32_t s_tmem = tmem + lane_off + 128 * t;
+        const uint32_t s_tmem = tmem + lane_off + 128 * t + 64 * hc;
         const uint32_t o_tmem = tmem + lane_off + 256 + 128 * t;
-        uint8_t* p_tile = smem + G::kP0 + t * kPBytes;
+        uint8_t* p_blk = smem + G::kP0 + t * kPBytes + hc * 16384;
+        float* xch = reinterpret_cast<float*>(smem + G::kX0) + t * (2 * 3 * kRows);  // [half][slot][row]
+        const uint32_t bar_id = 1 + t;
+        // O columns this half rescales / stores: 16-wide chunks [c_lo, c_hi)
+        constexpr int kOChunks = G::kDhPad / 16;
+        const int c_lo = hc ? (kOChunks + 1) / 2 : 0;
+        const int c_hi = hc ? kOChunks : (kOChunks + 1) / 2;
         const int T = p.n_k;
         const int group = p.packed ? row / T : 0;
         const int n_iter = p.packed ? 1 : n_kv;
         float m_run = -INFINITY, l_run = 0.f;
+        const uint32_t rsw = (uint32_t)(row & 7);
+        // shared-space address of this row in the P block and its 8 swizzled 16-byte chunks
+        const uint32_t p_row = smem_u32(p_blk) + (uint32_t)row * 128u;
 
         for (int j = 0; j < n_iter; ++j) {
             mbar_wait(&bars->s_full[t], j & 1);
             tc_fence_after();
-            float s[kKv];
-            PAB_TMEM_LD32(s_tmem + 0, (s + 0));
-            PAB_TMEM_LD32(s_tmem + 32, (s + 32));
-            PAB_TMEM_LD32(s_tmem + 64, (s + 64));
-            PAB_TMEM_LD32(s_tmem + 96, (s + 96));
-            tmem_wait_ld();
-            tc_fence_before();
-            mbar_arrive(&bars->s_free[t]);
-
-            // mask + tile max, in the log2 domain
-            float m_tile = -INFINITY;
+            // live score columns [lo, hi) of this row in this S tile
+            int lo = 0, hi = kKv;
             if (p.packed) {
-                const int lo = group * T, hi = lo + T;
-#pragma unroll
-                for (int c = 0; c < kKv; ++c) {
-                    const bool ok = (c >= lo) && (c < hi);
-                    s[c] = ok ? s[c] * p.scale_log2 : -INFINITY;
-                    m_tile = fmaxf(m_tile, s[c]);
-                }
-            } else {
-                const int valid = p.n_k - j * kKv;
-#pragma unroll
-                for (int c = 0; c < kKv; ++c) {
-                    s[c] = (c < valid) ? s[c] * p.scale_log2 : -INFINITY;
-                    m_tile = fmaxf(m_tile, s[c]);
-                }
+                lo = group * T;
+                hi = lo + T;
+            } else if (p.n_k - j * kKv < kKv) {
+                hi = p.n_k - j * kKv;
             }
+            // live columns of this thread's 64-column half, relative to the half
+            const int lo_c = max(lo - 64 * hc, 0), hi_c = min(hi - 64 * hc, 64);
+            const bool full = (lo_c == 0) && (hi_c == 64);
+            // ---- pass 1: this half's row max of the raw scores (scale > 0 commutes with max)
+            float mx = -INFINITY;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                float v[32];
+                PAB_TMEM_LD32(s_tmem + 32 * q, v);
+                tmem_wait_ld();
+                if (!full) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c)
+                        v[c] = (32 * q + c >= lo_c && 32 * q + c < hi_c) ? v[c] : -INFINITY;
+                }
+#pragma unroll
+                for (int w = 16; w >= 1; w >>= 1)
+#pragma unroll
+                    for (int c = 0; c < w; ++c) v[c] = fmaxf(v[c], v[c + w]);
+                mx = fmaxf(mx, v[0]);
+            }
+            // exchange with the other column half of the same rows (double-buffered slot)
+            const int slot = j & 1;
+            xch[(hc * 3 + slot) * kRows + row] = mx;
+            asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(kGroupThreads) : "memory");
+            mx = fmaxf(mx, xch[((1 - hc) * 3 + slot) * kRows + row]);
+            const float m_tile = mx * p.scale_log2;
             // previous P.V must be finished before P smem is overwritten or O rescaled
             if (j > 0) {
                 mbar_wait(&bars->o_done[t], (j - 1) & 1);
                 tc_fence_after();
             }
+            // both halves see identical (m_tile, m_run) per row, so they take the same branch
             const bool need = m_tile > m_run + 8.0f;
             if (__any_sync(0xffffffffu, need)) {
                 const float m_new = fmaxf(m_run, m_tile);
                 if (j > 0) {
                     const float alpha = fast_exp2(m_run - m_new);
                     l_run *= alpha;
-#pragma unroll
-                    for (int c0 = 0; c0 < G::kDhPad; c0 += 16) {
+                    for (int cc = c_lo; cc < c_hi; ++cc) {
                         float o[16];
-                        PAB_TMEM_LD16(o_tmem + c0, o);
+                        PAB_TMEM_LD16(o_tmem + 16 * cc, o);
                         tmem_wait_ld();
 #pragma unroll
                         for (int e = 0; e < 16; ++e) o[e] *= alpha;
-                        PAB_TMEM_ST16(o_tmem + c0, o);
+                        PAB_TMEM_ST16(o_tmem + 16 * cc, o);
                     }
                     tmem_wait_st();
                 }
                 m_run = m_new;
             }
-            const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-            // P = exp2(s - m), row sum, bf16 pack into the 128B-swizzled K-major tile
-            float sum = 0.f;
-            const uint32_t rsw = (uint32_t)(row & 7);
+            const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
+            // ---- pass 2: P = exp2(s * scale_log2 - m) -> bf16 into this half's 128B-swizzled P block
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int chunk = 0; chunk < kKv / 8; ++chunk) {
-                uint32_t packed4[4];
+            for (int q = 0; q < 2; ++q) {
+                float v[32];
+                PAB_TMEM_LD32(s_tmem + 32 * q, v);
+                tmem_wait_ld();
+                if (full) {
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float x0 = fast_exp2(s[chunk * 8 + 2 * e] - m_use);
-                    const float x1 = fast_exp2(s[chunk * 8 + 2 * e + 1] - m_use);
-                    sum += x0 + x1;
-                    __nv_bfloat162 b2 = __floats2bfloat162_rn(x0, x1);
-                    packed4[e] = *reinterpret_cast<uint32_t*>(&b2);
+                    for (int c = 0; c < 32; ++c) {
+                        v[c] = fast_exp2(fmaf(v[c], p.scale_log2, neg_m));
+                        acc[c & 3] += v[c];
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        const float e = fast_exp2(fmaf(v[c], p.scale_log2, neg_m));
+                        v[c] = (32 * q + c >= lo_c && 32 * q + c < hi_c) ? e : 0.f;
+                        acc[c & 3] += v[c];
+                    }
                 }
-                const int blk = chunk >> 3, cw = chunk & 7;
-                uint8_t* dst = p_tile + blk * 16384 + row * 128 + ((cw ^ rsw) << 4);
-                *reinterpret_cast<uint4*>(dst) = make_uint4(packed4[0], packed4[1], packed4[2], packed4[3]);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    st_shared_v4(p_row + ((((uint32_t)(q * 4 + k)) ^ rsw) << 4), pack_bf16(v[8 * k], v[8 * k + 1]),
+                                 pack_bf16(v[8 * k + 2], v[8 * k + 3]), pack_bf16(v[8 * k + 4], v[8 * k + 5]),
+                                 pack_bf16(v[8 * k + 6], v[8 * k + 7]));
             }
-            l_run += sum;
-            fence_async_smem();
             tc_fence_before();
+            mbar_arrive(&bars->s_free[t]);
+            l_run += (acc[0] + acc[1]) + (acc[2] + acc[3]);
+            fence_async_smem();
             mbar_arrive(&bars->p_full[t]);
         }
 
         // ------------------------------------------------------ epilogue
+        xch[(hc * 3 + 2) * kRows + row] = l_run;
+        asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(kGroupThreads) : "memory");
+        const float l_tot = l_run + xch[((1 - hc) * 3 + 2) * kRows + row];
         mbar_wait(&bars->o_done[t], (n_iter - 1) & 1);
         tc_fence_after();
         bool store = false;
         __nv_bfloat16* dst = nullptr;
         if (p.packed) {
-            const int b = b_base[t] + group, i = row - group * T;
+            const int b = b_base(t) + group, i = row - group * T;
             store = (group < p.packed) && (b < p.n_b) && (i < T);
             dst = p.o + (int64_t)a_idx * p.o_sa + (int64_t)b * p.o_sb + (int64_t)i * p.o_si + (int64_t)h * p.dh;
         } else {
-            const int i = i_base[t] + row;
+            const int i = i_base(t) + row;
             store = i < p.n_q;
-            dst = p.o + (int64_t)a_idx * p.o_sa + (int64_t)b_base[t] * p.o_sb + (int64_t)i * p.o_si +
+            dst = p.o + (int64_t)a_idx * p.o_sa + (int64_t)b_base(t) * p.o_sb + (int64_t)i * p.o_si +
                   (int64_t)h * p.dh;
         }
-        const float inv = (l_run > 0.f) ? 1.0f / l_run : 0.f;
-#pragma unroll
-        for (int c0 = 0; c0 < G::kDhPad; c0 += 16) {
+        const float inv = (l_tot > 0.f) ? 1.0f / l_tot : 0.f;
+        for (int cc = c_lo; cc < c_hi; ++cc) {
             float o[16];
-            PAB_TMEM_LD16(o_tmem + c0, o);
+            PAB_TMEM_LD16(o_tmem + 16 * cc, o);
             tmem_wait_ld();
             if (store) {
 #pragma unroll
                 for (int e = 0; e < 16; e += 8) {
-                    if (c0 + e < p.dh) {
+                    if (16 * cc + e < p.dh) {
                         uint32_t w[4];
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
                             __nv_bfloat162 b2 = __floats2bfloat162_rn(o[e + 2 * q] * inv, o[e + 2 * q + 1] * inv);
                             w[q] = *reinterpret_cast<uint32_t*>(&b2);
                         }
-                        *reinterpret_cast<uint4*>(dst + c0 + e) = make_uint4(w[0], w[1], w[2], w[3]);
+                        *reinterpret_cast<uint4*>(dst + 16 * cc + e) = make_uint4(w[0], w[1], w[2], w[3]);
                     }
                 }
             }
@@ -505,7 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
     }
     __syncthreads();
-    if (warp == 9) {
+    if (warp == kMmaWarp) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
     }
