@@ -132,6 +132,10 @@ int pab_attention(const pab_attn_args* args, int impl, void* stream);
  * (1 = tcgen05, 2 = SIMT).  Pure host logic, no GPU needed. */
 int pab_attention_select(const pab_attn_args* args);
 
+/* Debug only: record a clock64 event timeline of CTA (0,0,0) of subsequent
+ * tcgen05 attention launches into device_buffer (NULL disables). */
+int pab_attn_debug_trace(long long* device_buffer);
+
 #ifdef __cplusplus
 }
 #endif

@@ -63,6 +63,7 @@ SIGNATURES = {
     ),
     "pab_attention": (ctypes.c_int, [ctypes.POINTER(AttnArgs), ctypes.c_int, c_vp]),
     "pab_attention_select": (ctypes.c_int, [ctypes.POINTER(AttnArgs)]),
+    "pab_attn_debug_trace": (ctypes.c_int, [c_vp]),
 }
 
 

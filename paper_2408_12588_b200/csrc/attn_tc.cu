@@ -8,7 +8,8 @@
 //               tile, warps w and w+4 own the same 32 rows (TMEM lanes) and the
 //               left / right 64 score columns, exchanging the row max through smem
 //   warp  16    TMA producer (one elected lane)
-//   warp  17    TMEM allocator + MMA issuer (one elected lane)
+//   warps 17-18 MMA issuers, one per query tile, so the two tiles' tcgen05.mma
+//               streams are issued in parallel (warp 17 also owns TMEM)
 // Per KV tile j the MMA lane issues, ping-ponging the two query tiles,
 //   S_i = Q_i K_j^T  (M=128, N=128, K=dh padded to 16)  -> TMEM cols [128 i, 128 i + 128)
 //   O_i += P_i V_j   (M=128, N=64|16 blocks, K=128)      -> TMEM cols [256 + 128 i, ...)
@@ -36,8 +37,8 @@ namespace tc {
 
 constexpr int kSoftmaxWarps = 16;
 constexpr int kTmaWarp = 16;
-constexpr int kMmaWarp = 17;
-constexpr int kThreads = 32 * (kSoftmaxWarps + 2);
+constexpr int kMmaWarp = 17;  // MMA issuer for query tile 0 (also owns the TMEM allocation); 18 for tile 1
+constexpr int kThreads = 32 * (kSoftmaxWarps + 3);
 constexpr int kGroupThreads = 256;  // softmax threads per query tile
 constexpr int kRows = 128;       // query rows per tile == TMEM lanes
 constexpr int kKv = 128;         // keys per KV tile
@@ -52,7 +53,15 @@ struct Params {
     float scale_log2;  // scale * log2(e)
     __nv_bfloat16* o;
     int64_t o_sa, o_sb, o_si;
+    long long* trace;  // debug: clock64 event log of CTA (0,0,0), nullptr in production
 };
+
+// trace slot layout: [(j * 2 + t) * 16 + event]
+#define PAB_TRACE(cond, j, t, ev)                                                                   \
+    do {                                                                                            \
+        if (p.trace != nullptr && (cond) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) \
+            p.trace[((j) * 2 + (t)) * 16 + (ev)] = clock64();                                       \
+    } while (0)
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -69,13 +78,15 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    // try_wait with a suspend-time hint: the warp sleeps in hardware until the
+    // phase completes (or the hint expires) instead of spinning on issue slots
     const uint32_t addr = smem_u32(bar);
     asm volatile(
         "{\n\t.reg .pred done;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, %2;\n\t"
         "@!done bra WAIT_%=;\n}" ::"r"(addr),
-        "r"(parity)
+        "r"(parity), "r"(0x989680)
         : "memory");
 }
 // producer-side wait with a nanosleep backoff so a far-ahead TMA lane does not
@@ -246,13 +257,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     // ---------------------------------------------------------------- setup
     if (warp == kTmaWarp && lane == 0) {
-        prefetch_map(&q128); prefetch_map(&k128); prefetch_map(&v128);
-        if (N32) { prefetch_map(&q32); prefetch_map(&k32); prefetch_map(&v32); }
+        prefetch_map(&q128); prefetch_map(&k128); prefetch_map(&v32);
+        if (N32) { prefetch_map(&q32); prefetch_map(&k32); }
         mbar_init(&bars->q_full, 1);
         for (int s = 0; s < 2; ++s) {
             mbar_init(&bars->kv_full[s], 1);
             mbar_init(&bars->v_full[s], 1);
-            mbar_init(&bars->kv_empty[s], 1);
+            mbar_init(&bars->kv_empty[s], 2);  // released by both tiles' MMA warps
             mbar_init(&bars->s_full[s], 1);
             mbar_init(&bars->s_free[s], kGroupThreads);
             mbar_init(&bars->p_full[s], kGroupThreads);
@@ -307,115 +318,99 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int blk = 0; blk < N32; ++blk)
                     tma_load_5d(kd + N128 * 16384 + blk * 4096, &k32, &bars->kv_full[st], 64 * N128 + 16 * blk, h,
                                 kv_i, kv_b_eff, a_idx);
+                // V is staged as 16-column SW32 atoms ([atom][row][32 B]) so one
+                // MN-major descriptor spans the whole padded head dim (N = kDhPad)
                 mbar_expect_tx(&bars->v_full[st], box_bytes);
-                for (int blk = 0; blk < N128; ++blk)
-                    tma_load_5d(vd + blk * 16384, &v128, &bars->v_full[st], 64 * blk, h, kv_i, kv_b_eff, a_idx);
-                for (int blk = 0; blk < N32; ++blk)
-                    tma_load_5d(vd + N128 * 16384 + blk * 4096, &v32, &bars->v_full[st], 64 * N128 + 16 * blk, h,
-                                kv_i, kv_b_eff, a_idx);
+                for (int blk = 0; blk < G::kDhPad / 16; ++blk)
+                    tma_load_5d(vd + blk * 4096, &v32, &bars->v_full[st], 16 * blk, h, kv_i, kv_b_eff, a_idx);
             }
         }
-    } else if (warp == kMmaWarp) {
-        // ====================================================== MMA issuer (warp-wide)
-        {
-            constexpr uint32_t idS = idesc_bf16(128, 128, 0);
-            constexpr uint32_t idO64 = idesc_bf16(128, 64, 1);
-            constexpr uint32_t idO16 = idesc_bf16(128, 16, 1);
-            const uint32_t q_addr = smem_u32(smem + G::kQ0);
-            const uint32_t k_addr = smem_u32(smem + G::kK0);
-            const uint32_t v_addr = smem_u32(smem + G::kV0);
-            const uint32_t p_addr = smem_u32(smem + G::kP0);
-            mbar_wait(&bars->q_full, 0);
-            tc_fence_after();
-            // descriptors: constant layout bits | (address >> 4); moving the start
-            // address by `off` bytes adds off >> 4 to the low word (no carry: < 256 KB)
-            const uint64_t dq128 = smem_desc(q_addr, 16, 1024, kLayoutSW128);
-            const uint64_t dk128 = smem_desc(k_addr, 16, 1024, kLayoutSW128);
-            const uint64_t dq32 = smem_desc(q_addr + N128 * 16384, 16, 256, kLayoutSW32);
-            const uint64_t dk32 = smem_desc(k_addr + N128 * 16384, 16, 256, kLayoutSW32);
-            const uint64_t dp = smem_desc(p_addr, 16, 1024, kLayoutSW128);
-            const uint64_t dv128 = smem_desc(v_addr, 16, 1024, kLayoutSW128);
-            const uint64_t dv32 = smem_desc(v_addr + N128 * 16384, 16, 256, kLayoutSW32);
-            // S_t = Q_t K^T over the dh K-blocks
-            auto issue_s = [&](int t, int st) {
-                const uint32_t qo = (t * G::kTileBytes) >> 4, ko = (st * G::kTileBytes) >> 4;
-                const uint32_t d = tmem + 128 * t;
-                uint32_t acc = 0;
+    } else if (warp == kMmaWarp || warp == kMmaWarp + 1) {
+        // ============================ MMA issuer of query tile t (warp-wide, elected lane issues)
+        const int t = warp - kMmaWarp;
+        constexpr uint32_t idS = idesc_bf16(128, 128, 0);
+        constexpr uint32_t idO = idesc_bf16(128, G::kDhPad, 1);
+        const uint32_t q_addr = smem_u32(smem + G::kQ0 + t * G::kTileBytes);
+        const uint32_t k_addr = smem_u32(smem + G::kK0);
+        const uint32_t v_addr = smem_u32(smem + G::kV0);
+        const uint32_t p_addr = smem_u32(smem + G::kP0 + t * kPBytes);
+        const uint32_t d_s = tmem + 128 * t, d_o = tmem + 256 + 128 * t;
+        mbar_wait(&bars->q_full, 0);
+        tc_fence_after();
+        // descriptors: constant layout bits | (address >> 4); moving the start
+        // address by `off` bytes adds off >> 4 to the low word (no carry: < 256 KB)
+        const uint64_t dq128 = smem_desc(q_addr, 16, 1024, kLayoutSW128);
+        const uint64_t dk128 = smem_desc(k_addr, 16, 1024, kLayoutSW128);
+        const uint64_t dq32 = smem_desc(q_addr + N128 * 16384, 16, 256, kLayoutSW32);
+        const uint64_t dk32 = smem_desc(k_addr + N128 * 16384, 16, 256, kLayoutSW32);
+        const uint64_t dp = smem_desc(p_addr, 16, 1024, kLayoutSW128);
+        // V: MN-major SW32, 16-column atoms 4096 B apart (LBO), 8-row groups 256 B apart (SBO)
+        const uint64_t dv = smem_desc(v_addr, 4096, 256, kLayoutSW32);
+        // S_t = Q_t K^T over the dh K-blocks (K-major operands)
+        auto issue_s = [&](int st) {
+            const uint32_t ko = (st * G::kTileBytes) >> 4;
+            uint32_t acc = 0;
 #pragma unroll
-                for (int blk = 0; blk < N128; ++blk)
+            for (int blk = 0; blk < N128; ++blk)
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const uint32_t o = (blk * 16384 + 32 * k) >> 4;
-                        tc_mma(d, dq128 + qo + o, dk128 + ko + o, idS, acc);
-                        acc = 1;
-                    }
-#pragma unroll
-                for (int blk = 0; blk < N32; ++blk) {
-                    const uint32_t o = (blk * 4096) >> 4;
-                    tc_mma(d, dq32 + qo + o, dk32 + ko + o, idS, acc);
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t o = (blk * 16384 + 32 * k) >> 4;
+                    tc_mma(d_s, dq128 + o, dk128 + ko + o, idS, acc);
                     acc = 1;
                 }
-            };
-            // O_t += P_t V over 8 K-steps of 16 keys, per 64- / 16-wide dh block
-            auto issue_pv = [&](int t, int st, uint32_t accumulate) {
-                const uint32_t po = (t * kPBytes) >> 4, vo = (st * G::kTileBytes) >> 4;
-                const uint32_t d = tmem + 256 + 128 * t;
-#pragma unroll 2
-                for (int k = 0; k < kKv / 16; ++k) {
-                    const uint64_t a_desc = dp + po + (((k >> 2) * 16384 + 32 * (k & 3)) >> 4);
-                    const uint32_t acc = (accumulate || k > 0) ? 1u : 0u;
 #pragma unroll
-                    for (int blk = 0; blk < N128; ++blk)
-                        tc_mma(d + 64 * blk, a_desc, dv128 + vo + ((blk * 16384 + 2048 * k) >> 4), idO64, acc);
+            for (int blk = 0; blk < N32; ++blk) {
+                const uint32_t o = (blk * 4096) >> 4;
+                tc_mma(d_s, dq32 + o, dk32 + ko + o, idS, acc);
+                acc = 1;
+            }
+        };
+        // O_t += P_t V: 8 K-steps of 16 keys, each one N = kDhPad MMA
+        auto issue_pv = [&](int st, uint32_t accumulate) {
+            const uint32_t vo = (st * G::kTileBytes) >> 4;
 #pragma unroll
-                    for (int blk = 0; blk < N32; ++blk)
-                        tc_mma(d + 64 * N128 + 16 * blk, a_desc, dv32 + vo + ((blk * 4096 + 512 * k) >> 4), idO16, acc);
-                }
-            };
-            if (p.packed) {
-                // two independent single-tile problems: tile t uses KV stage t
-                for (int t = 0; t < 2; ++t) {
-                    mbar_wait(&bars->kv_full[t], 0);
+            for (int k = 0; k < kKv / 16; ++k)
+                tc_mma(d_o, dp + (((k >> 2) * 16384 + 32 * (k & 3)) >> 4), dv + vo + ((512 * k) >> 4), idO,
+                       (accumulate || k > 0) ? 1u : 0u);
+        };
+        if (p.packed) {
+            // independent single-tile problem: tile t uses KV stage t
+            mbar_wait(&bars->kv_full[t], 0);
+            tc_fence_after();
+            issue_s(t);
+            tc_commit(&bars->s_full[t]);
+            mbar_wait(&bars->v_full[t], 0);
+            mbar_wait(&bars->p_full[t], 0);
+            tc_fence_after();
+            issue_pv(t, 0);
+            tc_commit(&bars->o_done[t]);
+        } else {
+            mbar_wait(&bars->kv_full[0], 0);
+            tc_fence_after();
+            issue_s(0);
+            tc_commit(&bars->s_full[t]);
+            for (int j = 0; j < n_kv; ++j) {
+                const int st = j & 1;
+                // next scores first: S_t(j+1) only needs the softmax to have read S_t(j),
+                // so the tensor pipe computes it while P_t(j) is still being written
+                if (j + 1 < n_kv) {
+                    mbar_wait(&bars->kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+                    PAB_TRACE(lane == 0, j, t, 8);
+                    mbar_wait(&bars->s_free[t], j & 1);
                     tc_fence_after();
-                    issue_s(t, t);
+                    PAB_TRACE(lane == 0, j, t, 9);
+                    issue_s((j + 1) & 1);
                     tc_commit(&bars->s_full[t]);
                 }
-                for (int t = 0; t < 2; ++t) {
-                    mbar_wait(&bars->v_full[t], 0);
-                    mbar_wait(&bars->p_full[t], 0);
-                    tc_fence_after();
-                    issue_pv(t, t, 0);
-                    tc_commit(&bars->o_done[t]);
-                }
-            } else {
-                mbar_wait(&bars->kv_full[0], 0);
+                mbar_wait(&bars->v_full[st], (j >> 1) & 1);
+                PAB_TRACE(lane == 0, j, t, 10);
+                mbar_wait(&bars->p_full[t], j & 1);
                 tc_fence_after();
-                issue_s(0, 0);
-                tc_commit(&bars->s_full[0]);
-                issue_s(1, 0);
-                tc_commit(&bars->s_full[1]);
-                for (int j = 0; j < n_kv; ++j) {
-                    const int st = j & 1;
-                    const uint32_t ph = (j >> 1) & 1;
-                    mbar_wait(&bars->v_full[st], ph);
-                    for (int t = 0; t < 2; ++t) {
-                        mbar_wait(&bars->p_full[t], j & 1);
-                        tc_fence_after();
-                        issue_pv(t, st, j > 0);
-                        tc_commit(&bars->o_done[t]);
-                        if (j + 1 < n_kv) {
-                            const int st1 = (j + 1) & 1;
-                            if (t == 0) {
-                                mbar_wait(&bars->kv_full[st1], ((j + 1) >> 1) & 1);
-                            }
-                            mbar_wait(&bars->s_free[t], j & 1);
-                            tc_fence_after();
-                            issue_s(t, st1);
-                            tc_commit(&bars->s_full[t]);
-                        }
-                    }
-                    tc_commit(&bars->kv_empty[st]);
-                }
+                PAB_TRACE(lane == 0, j, t, 11);
+                issue_pv(st, j > 0);
+                tc_commit(&bars->o_done[t]);
+                PAB_TRACE(lane == 0, j, t, 12);
+                tc_commit(&bars->kv_empty[st]);
             }
         }
     } else {
@@ -443,8 +438,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t p_row = smem_u32(p_blk) + (uint32_t)row * 128u;
 
         for (int j = 0; j < n_iter; ++j) {
+            PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 0);
             mbar_wait(&bars->s_full[t], j & 1);
             tc_fence_after();
+            PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 1);
             // live score columns [lo, hi) of this row in this S tile
             int lo = 0, hi = kKv;
             if (p.packed) {
@@ -476,10 +473,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             // exchange with the other column half of the same rows (double-buffered slot)
             const int slot = j & 1;
+            PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 2);
             xch[(hc * 3 + slot) * kRows + row] = mx;
             asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(kGroupThreads) : "memory");
             mx = fmaxf(mx, xch[((1 - hc) * 3 + slot) * kRows + row]);
             const float m_tile = mx * p.scale_log2;
+            PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 3);
             // previous P.V must be finished before P smem is overwritten or O rescaled
             if (j > 0) {
                 mbar_wait(&bars->o_done[t], (j - 1) & 1);
@@ -505,6 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 m_run = m_new;
             }
             const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
+            PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 4);
             // ---- pass 2: P = exp2(s * scale_log2 - m) -> bf16 into this half's 128B-swizzled P block
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -536,6 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive(&bars->s_free[t]);
             l_run += (acc[0] + acc[1]) + (acc[2] + acc[3]);
             fence_async_smem();
+            PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 5);
             mbar_arrive(&bars->p_full[t]);
         }
 
@@ -616,6 +617,8 @@ bool make_map(CUtensorMap* map, const void* base, int dh, int heads, int n_i, in
     return r == CUDA_SUCCESS;
 }
 
+long long* g_trace = nullptr;  // set by pab_attn_debug_trace (debug builds of the timeline only)
+
 template <int N128, int N32>
 int launch(const pab_attn_args* a, int packed, cudaStream_t st) {
     using G = Geometry<N128, N32>;
@@ -647,6 +650,7 @@ int launch(const pab_attn_args* a, int packed, cudaStream_t st) {
     p.scale_log2 = a->scale * 1.4426950408889634f;
     p.o = reinterpret_cast<__nv_bfloat16*>(a->o);
     p.o_sa = a->o_sa; p.o_sb = a->o_sb; p.o_si = a->o_si;
+    p.trace = g_trace;
     dim3 grid;
     if (packed) {
         p.row_tiles = (a->n_b + packed - 1) / packed;
@@ -668,6 +672,11 @@ int packing_for(const pab_attn_args* a) {
 }
 
 }  // namespace tc
+
+extern "C" int pab_attn_debug_trace(long long* device_buffer) {
+    pab::tc::g_trace = device_buffer;
+    return PAB_OK;
+}
 
 bool attn_tc_supported(const pab_attn_args* a) {
     if (a->dh % 8 != 0 || a->dh > 96 || a->n_k < 1) return false;
