@@ -22,6 +22,8 @@ HEADERS = ["common.cuh", os.path.join("..", "..", "include", "pab_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
+# extra nvcc flags for kernel experiments, e.g. PAB_NVCC_FLAGS="-DPAB_POLY_EVERY=0"
+FLAGS += os.environ.get("PAB_NVCC_FLAGS", "").split()
 
 
 def _newest(paths):

@@ -57,11 +57,17 @@ struct Params {
 };
 
 // trace slot layout: [(j * 2 + t) * 16 + event]
+#ifndef PAB_ATTN_TRACE
+#define PAB_TRACE(cond, j, t, ev) \
+    do {                          \
+    } while (0)
+#else
 #define PAB_TRACE(cond, j, t, ev)                                                                   \
     do {                                                                                            \
         if (p.trace != nullptr && (cond) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) \
             p.trace[((j) * 2 + (t)) * 16 + (ev)] = clock64();                                       \
     } while (0)
+#endif
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -107,7 +113,13 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
     }
 }
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+#ifdef PAB_STS_VOLATILE
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+#else
+    // no memory clobber: lets the scheduler overlap the exp2 of the next chunk with
+    // this store (ordering w.r.t. the tensor core comes from fence.proxy.async + mbarrier)
+    asm("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d));
+#endif
 }
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 b2 = __floats2bfloat162_rn(lo, hi);
@@ -186,6 +198,67 @@ __device__ __forceinline__ float fast_exp2(float x) {
     return y;
 }
 
+// exp2 on the FMA/ALU pipes only (no FRND/F2I, which share the XU pipe with
+// MUFU.EX2): round-to-nearest via the 1.5*2^23 magic constant, then a degree-4
+// Taylor polynomial of 2^f on [-0.5, 0.5] (rel err < 5e-5, far below the bf16
+// rounding of P).  Used for a share of the scores so MUFU is not the only exp2
+// engine.  Inputs are clamped at -127 (x -> -inf gives ~0).
+__device__ __forceinline__ float poly_exp2(float x) {
+    x = fmaxf(x, -127.0f);
+    const float t = x + 12582912.0f;                 // 1.5 * 2^23: integer part lands in the low mantissa
+    const int xi = __float_as_int(t) - 0x4B400000;   // round(x)
+    const float f = x - (t - 12582912.0f);           // x - round(x) in [-0.5, 0.5]
+    float pf = fmaf(f, 0.009618129f, 0.05550411f);
+    pf = fmaf(pf, f, 0.2402265f);
+    pf = fmaf(pf, f, 0.6931472f);
+    pf = fmaf(pf, f, 1.0f);
+    return __int_as_float(__float_as_int(pf) + (xi << 23));
+}
+
+// Softmax building blocks, instantiated separately for full tiles (no masking
+// instructions at all) and for the partial / block-diagonal tiles.
+template <bool FULL>
+__device__ __forceinline__ float row_max_half(uint32_t s_tmem, int lo_c, int hi_c) {
+    float mx = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        float v[32];
+        PAB_TMEM_LD32(s_tmem + 32 * q, v);
+        tmem_wait_ld();
+        if (!FULL) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) v[c] = (32 * q + c >= lo_c && 32 * q + c < hi_c) ? v[c] : -INFINITY;
+        }
+#pragma unroll
+        for (int w = 16; w >= 1; w >>= 1)
+#pragma unroll
+            for (int c = 0; c < w; ++c) v[c] = fmaxf(v[c], v[c + w]);
+        mx = fmaxf(mx, v[0]);
+    }
+    return mx;
+}
+
+// P = exp2(s * scale_log2 - m) for this thread's 64 scores -> bf16 into its 128-byte
+// swizzled P row; returns the row-sum contribution.
+template <bool FULL>
+__device__ __forceinline__ float exp_pack_half(const float* v, float scale_log2, float neg_m, uint32_t p_row,
+                                               uint32_t rsw, int lo_c, int hi_c) {
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        float e[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            e[c] = fast_exp2(fmaf(v[8 * k + c], scale_log2, neg_m));
+            if (!FULL) e[c] = (8 * k + c >= lo_c && 8 * k + c < hi_c) ? e[c] : 0.f;
+            acc[c & 3] += e[c];
+        }
+        st_shared_v4(p_row + ((((uint32_t)k) ^ rsw) << 4), pack_bf16(e[0], e[1]), pack_bf16(e[2], e[3]),
+                     pack_bf16(e[4], e[5]), pack_bf16(e[6], e[7]));
+    }
+    return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
 // ------------------------------------------------------ UMMA descriptors
 // Shared-memory matrix descriptor (sm_100): start>>4 [0,14), LBO>>4 [16,30),
 // SBO>>4 [32,46), version=1 [46,48), base offset [49,52), layout [61,64).
@@ -213,18 +286,26 @@ struct Geometry {
     static constexpr int kDhPad = 64 * N128 + 16 * N32;
     static constexpr int kTileBytes = N128 * 16384 + N32 * 4096;  // one 128-row operand tile
     static constexpr int kQ0 = 0;
-    static constexpr int kK0 = 2 * kTileBytes;     // 2 K stages
-    static constexpr int kV0 = 4 * kTileBytes;     // 2 V stages
-    static constexpr int kP0 = 6 * kTileBytes;     // 2 P tiles
+    static constexpr int kK0 = 2 * kTileBytes;     // 3 K stages (K runs ahead of V: S(j+1) before PV(j))
+    static constexpr int kV0 = 5 * kTileBytes;     // 2 V stages
+    static constexpr int kP0 = 7 * kTileBytes;     // 2 P tiles
     static constexpr int kX0 = kP0 + 2 * kPBytes;  // row max / row sum exchange: [tile][half][slot][128] f32
     static constexpr int kBar = kX0 + 2 * 2 * 3 * kRows * 4;
     static constexpr int kSmem = kBar + 256 + 1024;  // + barriers + alignment slack
+    static_assert(kSmem <= 232448, "attention tiles exceed the 227 KB shared memory of one CTA");
 };
 
 struct Bars {
-    uint64_t q_full, kv_full[2], v_full[2], kv_empty[2], s_full[2], s_free[2], p_full[2], o_done[2];
+    uint64_t q_full, k_full[3], k_empty[3], v_full[2], v_empty[2], s_full[2], s_free[2], p_full[2], o_done[2];
     uint32_t tmem_base;
 };
+
+template <int N128, int N32>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap q128, const __grid_constant__ CUtensorMap q32,
+                   const __grid_constant__ CUtensorMap k128, const __grid_constant__ CUtensorMap k32,
+                   const __grid_constant__ CUtensorMap v128, const __grid_constant__ CUtensorMap v32,
+                   const Params p);
 
 template <int N128, int N32>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -260,10 +341,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         prefetch_map(&q128); prefetch_map(&k128); prefetch_map(&v32);
         if (N32) { prefetch_map(&q32); prefetch_map(&k32); }
         mbar_init(&bars->q_full, 1);
+        for (int s = 0; s < 3; ++s) {
+            mbar_init(&bars->k_full[s], 1);
+            mbar_init(&bars->k_empty[s], 2);  // released by both tiles' MMA warps
+        }
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&bars->kv_full[s], 1);
             mbar_init(&bars->v_full[s], 1);
-            mbar_init(&bars->kv_empty[s], 2);  // released by both tiles' MMA warps
+            mbar_init(&bars->v_empty[s], 2);  // released by both tiles' MMA warps
             mbar_init(&bars->s_full[s], 1);
             mbar_init(&bars->s_free[s], kGroupThreads);
             mbar_init(&bars->p_full[s], kGroupThreads);
@@ -281,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // packed tiles leave rows [box_rows, 128) of Q/K/V untouched by TMA:
         // zero them once so masked lanes can never inject NaN/Inf into P.V
         uint4 zero = make_uint4(0, 0, 0, 0);
-        for (int off = threadIdx.x * 16; off < 6 * G::kTileBytes; off += kThreads * 16)
+        for (int off = threadIdx.x * 16; off < 7 * G::kTileBytes; off += kThreads * 16)
             *reinterpret_cast<uint4*>(smem + off) = zero;
         fence_async_smem();
     }
@@ -303,26 +387,38 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tma_load_5d(dst + N128 * 16384 + blk * 4096, &q32, &bars->q_full, 64 * N128 + 16 * blk, h,
                                 i_base(t), b_base(t), a_idx);
             }
-            for (int j = 0; j < n_kv; ++j) {
-                const int st = j & 1;
-                if (j >= 2) mbar_wait_sleep(&bars->kv_empty[st], ((j >> 1) - 1) & 1);
-                const int kv_i = p.packed ? 0 : j * kKv;
-                // packed mode: each query tile owns its sequences, so KV tile j
-                // (j < 2) holds the keys of query tile j
-                const int kv_b_eff = b_base(j);
-                uint8_t* kd = smem + G::kK0 + st * G::kTileBytes;
-                uint8_t* vd = smem + G::kV0 + st * G::kTileBytes;
-                mbar_expect_tx(&bars->kv_full[st], box_bytes);
+            // packed mode: each query tile owns its sequences, so KV tile j (j < 2)
+            // holds the keys of query tile j
+            auto load_k = [&](int j) {
+                const int ks = j % 3;
+                if (j >= 3) mbar_wait(&bars->k_empty[ks], ((j / 3) - 1) & 1);
+                const int kv_i = p.packed ? 0 : j * kKv, kv_b = b_base(j);
+                uint8_t* kd = smem + G::kK0 + ks * G::kTileBytes;
+                mbar_expect_tx(&bars->k_full[ks], box_bytes);
                 for (int blk = 0; blk < N128; ++blk)
-                    tma_load_5d(kd + blk * 16384, &k128, &bars->kv_full[st], 64 * blk, h, kv_i, kv_b_eff, a_idx);
+                    tma_load_5d(kd + blk * 16384, &k128, &bars->k_full[ks], 64 * blk, h, kv_i, kv_b, a_idx);
                 for (int blk = 0; blk < N32; ++blk)
-                    tma_load_5d(kd + N128 * 16384 + blk * 4096, &k32, &bars->kv_full[st], 64 * N128 + 16 * blk, h,
-                                kv_i, kv_b_eff, a_idx);
-                // V is staged as 16-column SW32 atoms ([atom][row][32 B]) so one
-                // MN-major descriptor spans the whole padded head dim (N = kDhPad)
-                mbar_expect_tx(&bars->v_full[st], box_bytes);
+                    tma_load_5d(kd + N128 * 16384 + blk * 4096, &k32, &bars->k_full[ks], 64 * N128 + 16 * blk, h,
+                                kv_i, kv_b, a_idx);
+            };
+            // V is staged as 16-column SW32 atoms ([atom][row][32 B]) so one
+            // MN-major descriptor spans the whole padded head dim (N = kDhPad)
+            auto load_v = [&](int j) {
+                const int vs = j & 1;
+                if (j >= 2) mbar_wait(&bars->v_empty[vs], ((j >> 1) - 1) & 1);
+                const int kv_i = p.packed ? 0 : j * kKv, kv_b = b_base(j);
+                uint8_t* vd = smem + G::kV0 + vs * G::kTileBytes;
+                mbar_expect_tx(&bars->v_full[vs], box_bytes);
                 for (int blk = 0; blk < G::kDhPad / 16; ++blk)
-                    tma_load_5d(vd + blk * 4096, &v32, &bars->v_full[st], 16 * blk, h, kv_i, kv_b_eff, a_idx);
+                    tma_load_5d(vd + blk * 4096, &v32, &bars->v_full[vs], 16 * blk, h, kv_i, kv_b, a_idx);
+            };
+            // K runs up to two tiles ahead of V: S(j+1) is issued before PV(j)
+            load_k(0);
+            if (n_kv > 1) load_k(1);
+            load_v(0);
+            for (int j = 0; j < n_kv; ++j) {
+                if (j + 2 < n_kv) load_k(j + 2);
+                if (j + 1 < n_kv) load_v(j + 1);
             }
         }
     } else if (warp == kMmaWarp || warp == kMmaWarp + 1) {
@@ -375,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         if (p.packed) {
             // independent single-tile problem: tile t uses KV stage t
-            mbar_wait(&bars->kv_full[t], 0);
+            mbar_wait(&bars->k_full[t], 0);
             tc_fence_after();
             issue_s(t);
             tc_commit(&bars->s_full[t]);
@@ -385,22 +481,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             issue_pv(t, 0);
             tc_commit(&bars->o_done[t]);
         } else {
-            mbar_wait(&bars->kv_full[0], 0);
+            mbar_wait(&bars->k_full[0], 0);
             tc_fence_after();
             issue_s(0);
             tc_commit(&bars->s_full[t]);
+            tc_commit(&bars->k_empty[0]);
             for (int j = 0; j < n_kv; ++j) {
                 const int st = j & 1;
                 // next scores first: S_t(j+1) only needs the softmax to have read S_t(j),
                 // so the tensor pipe computes it while P_t(j) is still being written
                 if (j + 1 < n_kv) {
-                    mbar_wait(&bars->kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+                    mbar_wait(&bars->k_full[(j + 1) % 3], ((j + 1) / 3) & 1);
                     PAB_TRACE(lane == 0, j, t, 8);
                     mbar_wait(&bars->s_free[t], j & 1);
                     tc_fence_after();
                     PAB_TRACE(lane == 0, j, t, 9);
-                    issue_s((j + 1) & 1);
+                    issue_s((j + 1) % 3);
                     tc_commit(&bars->s_full[t]);
+                    tc_commit(&bars->k_empty[(j + 1) % 3]);
                 }
                 mbar_wait(&bars->v_full[st], (j >> 1) & 1);
                 PAB_TRACE(lane == 0, j, t, 10);
@@ -410,7 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 issue_pv(st, j > 0);
                 tc_commit(&bars->o_done[t]);
                 PAB_TRACE(lane == 0, j, t, 12);
-                tc_commit(&bars->kv_empty[st]);
+                tc_commit(&bars->v_empty[st]);
             }
         }
     } else {
@@ -454,23 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int lo_c = max(lo - 64 * hc, 0), hi_c = min(hi - 64 * hc, 64);
             const bool full = (lo_c == 0) && (hi_c == 64);
             // ---- pass 1: this half's row max of the raw scores (scale > 0 commutes with max)
-            float mx = -INFINITY;
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                float v[32];
-                PAB_TMEM_LD32(s_tmem + 32 * q, v);
-                tmem_wait_ld();
-                if (!full) {
-#pragma unroll
-                    for (int c = 0; c < 32; ++c)
-                        v[c] = (32 * q + c >= lo_c && 32 * q + c < hi_c) ? v[c] : -INFINITY;
-                }
-#pragma unroll
-                for (int w = 16; w >= 1; w >>= 1)
-#pragma unroll
-                    for (int c = 0; c < w; ++c) v[c] = fmaxf(v[c], v[c + w]);
-                mx = fmaxf(mx, v[0]);
-            }
+            float mx = full ? row_max_half<true>(s_tmem, 0, 64) : row_max_half<false>(s_tmem, lo_c, hi_c);
             // exchange with the other column half of the same rows (double-buffered slot)
             const int slot = j & 1;
             PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 2);
@@ -505,36 +587,29 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
             PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 4);
-            // ---- pass 2: P = exp2(s * scale_log2 - m) -> bf16 into this half's 128B-swizzled P block
-            float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                float v[32];
-                PAB_TMEM_LD32(s_tmem + 32 * q, v);
-                tmem_wait_ld();
-                if (full) {
-#pragma unroll
-                    for (int c = 0; c < 32; ++c) {
-                        v[c] = fast_exp2(fmaf(v[c], p.scale_log2, neg_m));
-                        acc[c & 3] += v[c];
-                    }
-                } else {
-#pragma unroll
-                    for (int c = 0; c < 32; ++c) {
-                        const float e = fast_exp2(fmaf(v[c], p.scale_log2, neg_m));
-                        v[c] = (32 * q + c >= lo_c && 32 * q + c < hi_c) ? e : 0.f;
-                        acc[c & 3] += v[c];
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    st_shared_v4(p_row + ((((uint32_t)(q * 4 + k)) ^ rsw) << 4), pack_bf16(v[8 * k], v[8 * k + 1]),
-                                 pack_bf16(v[8 * k + 2], v[8 * k + 3]), pack_bf16(v[8 * k + 4], v[8 * k + 5]),
-                                 pack_bf16(v[8 * k + 6], v[8 * k + 7]));
-            }
+            // ---- pass 2: P = exp2(s * scale_log2 - m) -> bf16 into this half's 128B-swizzled P block.
+            // All 64 scores are pulled from TMEM first so S can be released (s_free) and the
+            // tensor pipe can start S(j+1) while this warp is still exponentiating.
+            float v[64];
+            PAB_TMEM_LD32(s_tmem, v);
+            PAB_TMEM_LD32(s_tmem + 32, (v + 32));
+            tmem_wait_ld();
+            PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 6);
             tc_fence_before();
             mbar_arrive(&bars->s_free[t]);
-            l_run += (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#ifndef PAB_NO_MUFU_TOKEN
+            // MUFU token: the two query tiles' exp2 phases strictly alternate
+            // (tile 0 of step j, tile 1 of step j, tile 0 of step j+1, ...), so one
+            // group exponentiates while the other reduces / exchanges / waits.
+            if (t == 1 || j > 0) asm volatile("bar.sync %0, %1;" ::"r"(3 + t), "r"(2 * kGroupThreads) : "memory");
+#endif
+            const float psum = full ? exp_pack_half<true>(v, p.scale_log2, neg_m, p_row, rsw, 0, 64)
+                                    : exp_pack_half<false>(v, p.scale_log2, neg_m, p_row, rsw, lo_c, hi_c);
+#ifndef PAB_NO_MUFU_TOKEN
+            if (t == 0 || j + 1 < n_iter) asm volatile("bar.arrive %0, %1;" ::"r"(4 - t), "r"(2 * kGroupThreads) : "memory");
+#endif
+            PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 7);
+            l_run += psum;
             fence_async_smem();
             PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 5);
             mbar_arrive(&bars->p_full[t]);
@@ -679,7 +754,7 @@ extern "C" int pab_attn_debug_trace(long long* device_buffer) {
 }
 
 bool attn_tc_supported(const pab_attn_args* a) {
-    if (a->dh % 8 != 0 || a->dh > 96 || a->n_k < 1) return false;
+    if (a->dh % 8 != 0 || a->dh > 80 || a->n_k < 1) return false;  // smem: 7 operand tiles + 2 P tiles
     const int64_t strides[] = {a->q_sa, a->q_sb, a->q_si, a->k_sa, a->k_sb, a->k_si,
                                a->v_sa, a->v_sb, a->v_si, a->o_si};
     for (int64_t s : strides)
@@ -699,7 +774,7 @@ int attn_tc_launch(const pab_attn_args* a, cudaStream_t st) {
 #define PAB_TC(A, B) \
     if (n128 == A && n32 == B) return tc::launch<A, B>(a, packed, st)
     PAB_TC(0, 1); PAB_TC(0, 2); PAB_TC(0, 3);
-    PAB_TC(1, 0); PAB_TC(1, 1); PAB_TC(1, 2);
+    PAB_TC(1, 0); PAB_TC(1, 1);
 #undef PAB_TC
     return PAB_ERR_UNSUPPORTED;
 }

@@ -26,7 +26,7 @@ torch.cuda.synchronize()
 lib.pab_attn_debug_trace(None)
 tr = buf.view(n_kv, 2, 16).cpu()
 t0 = int(tr[tr > 0].min())
-names = {0: "sm:wait_S", 1: "sm:S_ready", 2: "sm:pass1_done", 3: "sm:xchg_done", 4: "sm:o_done/resc", 5: "sm:P_written",
+names = {0: "sm:wait_S", 1: "sm:S_ready", 2: "sm:pass1_done", 3: "sm:xchg_done", 4: "sm:o_done/resc", 5: "sm:P_written", 6: "sm:pass2_loaded", 7: "sm:pass2_exp_done",
          8: "mma:wait_sfree", 9: "mma:sfree_ok", 10: "mma:wait_P", 11: "mma:P_ok", 12: "mma:PV_issued"}
 ev = []
 for j in range(n_kv):
@@ -35,5 +35,6 @@ for j in range(n_kv):
             v = int(tr[j, t, e])
             if v:
                 ev.append((v - t0, j, t, nm))
+WARPS = os.environ.get('TL_ALL')
 for v, j, t, nm in sorted(ev):
     print(f"{v:8d}  j={j:2d} t={t}  {nm}")
