@@ -215,6 +215,11 @@ __device__ __forceinline__ float poly_exp2(float x) {
     return __int_as_float(__float_as_int(pf) + (xi << 23));
 }
 
+#ifndef PAB_POLY_EVERY
+#define PAB_POLY_EVERY 8
+#endif
+#define PAB_POLY_DIV (PAB_POLY_EVERY > 0 ? PAB_POLY_EVERY : 1)
+
 // Softmax building blocks, instantiated separately for full tiles (no masking
 // instructions at all) and for the partial / block-diagonal tiles.
 template <bool FULL>
@@ -238,11 +243,55 @@ __device__ __forceinline__ float row_max_half(uint32_t s_tmem, int lo_c, int hi_
     return mx;
 }
 
+// packed fp32x2 helpers (Blackwell FFMA2 / FADD2: two lanes of work per issue slot)
+__device__ __forceinline__ unsigned long long f2_pack(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float2 f2_unpack(unsigned long long r) {
+    float2 v;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+    return v;
+}
+__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b,
+                                                     unsigned long long c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ unsigned long long f2_add(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
 // P = exp2(s * scale_log2 - m) for this thread's 64 scores -> bf16 into its 128-byte
 // swizzled P row; returns the row-sum contribution.
 template <bool FULL>
 __device__ __forceinline__ float exp_pack_half(const float* v, float scale_log2, float neg_m, uint32_t p_row,
                                                uint32_t rsw, int lo_c, int hi_c) {
+    if (FULL) {
+        const unsigned long long sc2 = f2_pack(scale_log2, scale_log2), nm2 = f2_pack(neg_m, neg_m);
+        unsigned long long acc2[2] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            float e[8];
+#pragma unroll
+            for (int c = 0; c < 8; c += 2) {
+                const float2 x = f2_unpack(f2_fma(f2_pack(v[8 * k + c], v[8 * k + c + 1]), sc2, nm2));
+                e[c] = fast_exp2(x.x);
+                // optionally every PAB_POLY_EVERY-th score on the FMA pipe (polynomial exp2)
+                e[c + 1] = (PAB_POLY_EVERY > 0 && ((c + 1) % PAB_POLY_DIV) == PAB_POLY_DIV - 1) ? poly_exp2(x.y)
+                                                                                               : fast_exp2(x.y);
+                acc2[(c >> 1) & 1] = f2_add(acc2[(c >> 1) & 1], f2_pack(e[c], e[c + 1]));
+            }
+            st_shared_v4(p_row + ((((uint32_t)k) ^ rsw) << 4), pack_bf16(e[0], e[1]), pack_bf16(e[2], e[3]),
+                         pack_bf16(e[4], e[5]), pack_bf16(e[6], e[7]));
+        }
+        const float2 a0 = f2_unpack(acc2[0]), a1 = f2_unpack(acc2[1]);
+        return (a0.x + a0.y) + (a1.x + a1.y);
+    }
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -250,7 +299,7 @@ __device__ __forceinline__ float exp_pack_half(const float* v, float scale_log2,
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
             e[c] = fast_exp2(fmaf(v[8 * k + c], scale_log2, neg_m));
-            if (!FULL) e[c] = (8 * k + c >= lo_c && 8 * k + c < hi_c) ? e[c] : 0.f;
+            e[c] = (8 * k + c >= lo_c && 8 * k + c < hi_c) ? e[c] : 0.f;
             acc[c & 3] += e[c];
         }
         st_shared_v4(p_row + ((((uint32_t)k) ^ rsw) << 4), pack_bf16(e[0], e[1]), pack_bf16(e[2], e[3]),
