@@ -136,6 +136,82 @@ __global__ void __launch_bounds__(256) residual_modnorm_kernel(
     }
 }
 
+// Exact-width variant (D == 128 * NV): no per-element guards, every load of the
+// row (x and all pending terms) issued before any arithmetic, streaming cache
+// hints (each byte is touched once).  One warp per row.
+template <int NV>
+__global__ void __launch_bounds__(256) residual_modnorm_exact_kernel(
+    const float* __restrict__ x_in, float* __restrict__ x_out, PendingList pend,
+    const float* __restrict__ gamma, const float* __restrict__ beta,
+    const float* __restrict__ mod, __nv_bfloat16* __restrict__ h_out,
+    int64_t rows, float eps, int mode, int write_x, RowPerm perm) {
+    constexpr int D = 128 * NV;
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (row >= rows) return;
+    const int64_t base = row * (int64_t)D;
+    float4 v[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) v[j] = __ldcs(reinterpret_cast<const float4*>(x_in + base) + j * 32 + lane);
+#pragma unroll
+    for (int p = 0; p < PAB_MAX_PENDING; ++p) {
+        if (p < pend.n) {
+            uint2 raw[NV];
+#pragma unroll
+            for (int j = 0; j < NV; ++j) raw[j] = __ldcs(reinterpret_cast<const uint2*>(pend.p[p] + base) + j * 32 + lane);
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                const float2 a = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&raw[j].x));
+                const float2 b = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&raw[j].y));
+                v[j].x += a.x; v[j].y += a.y; v[j].z += b.x; v[j].w += b.y;
+            }
+        }
+    }
+    if (write_x) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) __stcs(reinterpret_cast<float4*>(x_out + base) + j * 32 + lane, v[j]);
+    }
+    if (mode == 0) return;
+    __nv_bfloat16* hrow = h_out + perm.map(row) * (int64_t)D;
+    auto store_h = [&](int j, float a, float b, float c, float d) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+        uint2 raw;
+        raw.x = *reinterpret_cast<uint32_t*>(&lo);
+        raw.y = *reinterpret_cast<uint32_t*>(&hi);
+        __stcs(reinterpret_cast<uint2*>(hrow) + j * 32 + lane, raw);
+    };
+    if (mode == 2) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) store_h(j, v[j].x, v[j].y, v[j].z, v[j].w);
+        return;
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+    const float mean = warp_sum(s) * (1.0f / (float)D);
+    float q = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        v[j].x -= mean; v[j].y -= mean; v[j].z -= mean; v[j].w -= mean;
+        q += (v[j].x * v[j].x + v[j].y * v[j].y) + (v[j].z * v[j].z + v[j].w * v[j].w);
+    }
+    const float inv = 1.0f / sqrtf(warp_sum(q) * (1.0f / (float)D) + eps);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        const int c = (j * 32 + lane) * 4;
+        const float4 sh = __ldg(reinterpret_cast<const float4*>(mod + c));
+        const float4 sc = __ldg(reinterpret_cast<const float4*>(mod + D + c));
+        float4 hv = make_float4(v[j].x * inv, v[j].y * inv, v[j].z * inv, v[j].w * inv);
+        if (gamma) {
+            const float4 g = __ldg(reinterpret_cast<const float4*>(gamma + c));
+            const float4 bb = __ldg(reinterpret_cast<const float4*>(beta + c));
+            hv = make_float4(hv.x * g.x + bb.x, hv.y * g.y + bb.y, hv.z * g.z + bb.z, hv.w * g.w + bb.w);
+        }
+        store_h(j, hv.x * (1.0f + sc.x) + sh.x, hv.y * (1.0f + sc.y) + sh.y, hv.z * (1.0f + sc.z) + sh.z,
+                hv.w * (1.0f + sc.w) + sh.w);
+    }
+}
+
 template <int VEC>
 static int launch_modnorm_vec(const float* x_in, float* x_out, const PendingList& pl,
                               const float* gamma, const float* beta, const float* mod,
@@ -144,6 +220,21 @@ static int launch_modnorm_vec(const float* x_in, float* x_out, const PendingList
     const int per_lane = (D + 32 * VEC - 1) / (32 * VEC);
     const int warps = 8;
     dim3 grid((unsigned)((rows + warps - 1) / warps)), block(32 * warps);
+    if (VEC == 4 && D % 128 == 0 && (mod == nullptr || (uintptr_t)mod % 16 == 0)) {
+#define PAB_MNX(NVV)                                                                                       \
+    residual_modnorm_exact_kernel<NVV><<<grid, block, 0, st>>>(x_in, x_out, pl, gamma, beta, mod, h, rows, eps, \
+                                                                mode, write_x, perm)
+        switch (D / 128) {
+            case 1: PAB_MNX(1); return launch_status("residual_modnorm");
+            case 2: PAB_MNX(2); return launch_status("residual_modnorm");
+            case 4: PAB_MNX(4); return launch_status("residual_modnorm");
+            case 8: PAB_MNX(8); return launch_status("residual_modnorm");
+            case 9: PAB_MNX(9); return launch_status("residual_modnorm");
+            case 12: PAB_MNX(12); return launch_status("residual_modnorm");
+            default: break;
+        }
+#undef PAB_MNX
+    }
 #define PAB_MN(NVV)                                                                       \
     residual_modnorm_kernel<VEC, NVV><<<grid, block, 0, st>>>(x_in, x_out, pl, gamma, beta, \
                                                               mod, h, rows, D, eps, mode, write_x, perm)
