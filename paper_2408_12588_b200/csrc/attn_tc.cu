@@ -50,6 +50,8 @@ struct Params {
     int packed;        // 0: rows along i; >0: sequences per tile (T = n_k)
     int row_tiles;     // query tiles along the tiled axis
     int n_kv;          // KV tiles per problem
+    int n_pairs;       // query-tile pairs per (problem, head)
+    int n_items;       // total work items = n_pairs * heads * problems
     float scale_log2;  // scale * log2(e)
     __nv_bfloat16* o;
     int64_t o_sa, o_sb, o_si;
@@ -345,17 +347,16 @@ struct Geometry {
 };
 
 struct Bars {
-    uint64_t q_full, k_full[3], k_empty[3], v_full[2], v_empty[2], s_full[2], s_free[2], p_full[2], o_done[2];
+    uint64_t q_full, q_empty, k_full[3], k_empty[3], v_full[2], v_empty[2];
+    uint64_t s_full[2], s_free[2], p_full[2], o_done[2], o_free[2];
     uint32_t tmem_base;
 };
 
-template <int N128, int N32>
-__global__ void __launch_bounds__(kThreads, 1)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap q128, const __grid_constant__ CUtensorMap q32,
-                   const __grid_constant__ CUtensorMap k128, const __grid_constant__ CUtensorMap k32,
-                   const __grid_constant__ CUtensorMap v128, const __grid_constant__ CUtensorMap v32,
-                   const Params p);
-
+// Persistent kernel: grid = min(#items, #SMs); CTA c processes work items
+// c, c + gridDim.x, ...  An item is two 128-row query tiles of one (problem,
+// head); all pipeline stages / barrier phases run on CTA-global counters so
+// the producer prefetches the next item's Q and K/V while the current one
+// finishes.
 template <int N128, int N32>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap q128, const __grid_constant__ CUtensorMap q32,
@@ -368,28 +369,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     Bars* bars = reinterpret_cast<Bars*>(smem + G::kBar);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int pair = blockIdx.x, h = blockIdx.y, az = blockIdx.z;
-    // problem coordinates of the two query tiles
-    // problem coordinates of the two query tiles (t = 0, 1); kept as scalar
-    // expressions so no local-memory array is indexed by a runtime t
-    int a_idx, b_idx0;
-    if (p.packed) {
-        a_idx = az;
-        b_idx0 = 0;
-    } else {
-        a_idx = az / p.n_b;
-        b_idx0 = az - a_idx * p.n_b;
-    }
-    auto i_base = [&](int t) { return p.packed ? 0 : (2 * pair + t) * kRows; };
-    auto b_base = [&](int t) { return p.packed ? (2 * pair + t) * p.packed : b_idx0; };
+    // item -> (head, pair, a, b), head fastest: concurrently running CTAs read all heads of
+    // the same q/k/v rows (whole 6.9 KB qkv rows per DRAM page visit) and share K/V in L2
+    struct Item {
+        int pair, h, a_idx, b_idx0;
+    };
+    auto decode = [&](int item) {
+        Item it;
+        it.h = item % p.heads;
+        const int rest = item / p.heads;
+        it.pair = rest % p.n_pairs;
+        const int az = rest / p.n_pairs;
+        if (p.packed) {
+            it.a_idx = az;
+            it.b_idx0 = 0;
+        } else {
+            it.a_idx = az / p.n_b;
+            it.b_idx0 = az - it.a_idx * p.n_b;
+        }
+        return it;
+    };
+    // per-tile coordinates (t = 0, 1) as scalar expressions (no runtime-indexed arrays)
+    auto i_base = [&](const Item& it, int t) { return p.packed ? 0 : (2 * it.pair + t) * kRows; };
+    auto b_base = [&](const Item& it, int t) { return p.packed ? (2 * it.pair + t) * p.packed : it.b_idx0; };
     const int box_rows = p.packed ? p.packed * p.n_k : kRows;  // rows a TMA box fills
     const uint32_t box_bytes = (uint32_t)box_rows * (uint32_t)(N128 * 128 + N32 * 32);
+    const int n_iter = p.packed ? 1 : p.n_kv;                  // S/P/O iterations per item and tile
+    const int kv_per_item = p.packed ? 2 : p.n_kv;             // K (and V) tiles loaded per item
+    const int my_items = (p.n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
 
     // ---------------------------------------------------------------- setup
     if (warp == kTmaWarp && lane == 0) {
         prefetch_map(&q128); prefetch_map(&k128); prefetch_map(&v32);
         if (N32) { prefetch_map(&q32); prefetch_map(&k32); }
         mbar_init(&bars->q_full, 1);
+        mbar_init(&bars->q_empty, 2);  // both tiles' MMA warps are done with Q
         for (int s = 0; s < 3; ++s) {
             mbar_init(&bars->k_full[s], 1);
             mbar_init(&bars->k_empty[s], 2);  // released by both tiles' MMA warps
@@ -401,6 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&bars->s_free[s], kGroupThreads);
             mbar_init(&bars->p_full[s], kGroupThreads);
             mbar_init(&bars->o_done[s], 1);
+            mbar_init(&bars->o_free[s], kGroupThreads);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -422,52 +437,57 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = bars->tmem_base;
-    const int n_kv = p.n_kv;
 
     if (warp == kTmaWarp) {
         // ===================================================== TMA producer
         if (lane == 0) {
-            mbar_expect_tx(&bars->q_full, 2 * box_bytes);
-            for (int t = 0; t < 2; ++t) {
-                uint8_t* dst = smem + G::kQ0 + t * G::kTileBytes;
-                for (int blk = 0; blk < N128; ++blk)
-                    tma_load_5d(dst + blk * 16384, &q128, &bars->q_full, 64 * blk, h, i_base(t), b_base(t), a_idx);
-                for (int blk = 0; blk < N32; ++blk)
-                    tma_load_5d(dst + N128 * 16384 + blk * 4096, &q32, &bars->q_full, 64 * N128 + 16 * blk, h,
-                                i_base(t), b_base(t), a_idx);
-            }
-            // packed mode: each query tile owns its sequences, so KV tile j (j < 2)
-            // holds the keys of query tile j
-            auto load_k = [&](int j) {
-                const int ks = j % 3;
-                if (j >= 3) mbar_wait(&bars->k_empty[ks], ((j / 3) - 1) & 1);
-                const int kv_i = p.packed ? 0 : j * kKv, kv_b = b_base(j);
+            // K ring (3 stages) runs up to two tiles ahead of the V ring (2 stages): S(j+1) is issued before PV(j)
+            auto load_k = [&](const Item& it, int g, int j) {
+                const int ks = g % 3;
+                if (g >= 3) mbar_wait(&bars->k_empty[ks], ((g / 3) - 1) & 1);
+                const int kv_i = p.packed ? 0 : j * kKv, kv_b = b_base(it, p.packed ? j : 0);
                 uint8_t* kd = smem + G::kK0 + ks * G::kTileBytes;
                 mbar_expect_tx(&bars->k_full[ks], box_bytes);
                 for (int blk = 0; blk < N128; ++blk)
-                    tma_load_5d(kd + blk * 16384, &k128, &bars->k_full[ks], 64 * blk, h, kv_i, kv_b, a_idx);
+                    tma_load_5d(kd + blk * 16384, &k128, &bars->k_full[ks], 64 * blk, it.h, kv_i, kv_b, it.a_idx);
                 for (int blk = 0; blk < N32; ++blk)
-                    tma_load_5d(kd + N128 * 16384 + blk * 4096, &k32, &bars->k_full[ks], 64 * N128 + 16 * blk, h,
-                                kv_i, kv_b, a_idx);
+                    tma_load_5d(kd + N128 * 16384 + blk * 4096, &k32, &bars->k_full[ks], 64 * N128 + 16 * blk, it.h,
+                                kv_i, kv_b, it.a_idx);
             };
             // V is staged as 16-column SW32 atoms ([atom][row][32 B]) so one
             // MN-major descriptor spans the whole padded head dim (N = kDhPad)
-            auto load_v = [&](int j) {
-                const int vs = j & 1;
-                if (j >= 2) mbar_wait(&bars->v_empty[vs], ((j >> 1) - 1) & 1);
-                const int kv_i = p.packed ? 0 : j * kKv, kv_b = b_base(j);
+            auto load_v = [&](const Item& it, int g, int j) {
+                const int vs = g & 1;
+                if (g >= 2) mbar_wait(&bars->v_empty[vs], ((g >> 1) - 1) & 1);
+                const int kv_i = p.packed ? 0 : j * kKv, kv_b = b_base(it, p.packed ? j : 0);
                 uint8_t* vd = smem + G::kV0 + vs * G::kTileBytes;
                 mbar_expect_tx(&bars->v_full[vs], box_bytes);
                 for (int blk = 0; blk < G::kDhPad / 16; ++blk)
-                    tma_load_5d(vd + blk * 4096, &v32, &bars->v_full[vs], 16 * blk, h, kv_i, kv_b, a_idx);
+                    tma_load_5d(vd + blk * 4096, &v32, &bars->v_full[vs], 16 * blk, it.h, kv_i, kv_b, it.a_idx);
             };
-            // K runs up to two tiles ahead of V: S(j+1) is issued before PV(j)
-            load_k(0);
-            if (n_kv > 1) load_k(1);
-            load_v(0);
-            for (int j = 0; j < n_kv; ++j) {
-                if (j + 2 < n_kv) load_k(j + 2);
-                if (j + 1 < n_kv) load_v(j + 1);
+            int gkv = 0;  // K/V tiles loaded so far by this CTA
+            for (int c = 0; c < my_items; ++c) {
+                const Item it = decode((int)blockIdx.x + c * (int)gridDim.x);
+                if (c > 0) mbar_wait(&bars->q_empty, (c - 1) & 1);
+                mbar_expect_tx(&bars->q_full, 2 * box_bytes);
+                for (int t = 0; t < 2; ++t) {
+                    uint8_t* dst = smem + G::kQ0 + t * G::kTileBytes;
+                    for (int blk = 0; blk < N128; ++blk)
+                        tma_load_5d(dst + blk * 16384, &q128, &bars->q_full, 64 * blk, it.h, i_base(it, t),
+                                    b_base(it, t), it.a_idx);
+                    for (int blk = 0; blk < N32; ++blk)
+                        tma_load_5d(dst + N128 * 16384 + blk * 4096, &q32, &bars->q_full, 64 * N128 + 16 * blk, it.h,
+                                    i_base(it, t), b_base(it, t), it.a_idx);
+                }
+                // packed: KV tile j (j < 2) holds the keys of query tile j
+                load_k(it, gkv, 0);
+                if (kv_per_item > 1) load_k(it, gkv + 1, 1);
+                load_v(it, gkv, 0);
+                for (int j = 0; j < kv_per_item; ++j) {
+                    if (j + 2 < kv_per_item) load_k(it, gkv + j + 2, j + 2);
+                    if (j + 1 < kv_per_item) load_v(it, gkv + j + 1, j + 1);
+                }
+                gkv += kv_per_item;
             }
         }
     } else if (warp == kMmaWarp || warp == kMmaWarp + 1) {
@@ -480,8 +500,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t v_addr = smem_u32(smem + G::kV0);
         const uint32_t p_addr = smem_u32(smem + G::kP0 + t * kPBytes);
         const uint32_t d_s = tmem + 128 * t, d_o = tmem + 256 + 128 * t;
-        mbar_wait(&bars->q_full, 0);
-        tc_fence_after();
         // descriptors: constant layout bits | (address >> 4); moving the start
         // address by `off` bytes adds off >> 4 to the low word (no carry: < 256 KB)
         const uint64_t dq128 = smem_desc(q_addr, 16, 1024, kLayoutSW128);
@@ -518,47 +536,41 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_mma(d_o, dp + (((k >> 2) * 16384 + 32 * (k & 3)) >> 4), dv + vo + ((512 * k) >> 4), idO,
                        (accumulate || k > 0) ? 1u : 0u);
         };
-        if (p.packed) {
-            // independent single-tile problem: tile t uses KV stage t
-            mbar_wait(&bars->k_full[t], 0);
+        // S for global iteration gi from K ring slot g; the softmax must have released S(gi - 1)
+        auto do_s = [&](int gi, int g) {
+            mbar_wait(&bars->k_full[g % 3], (g / 3) & 1);
+            if (gi > 0) mbar_wait(&bars->s_free[t], (gi - 1) & 1);
             tc_fence_after();
-            issue_s(t);
+            issue_s(g % 3);
             tc_commit(&bars->s_full[t]);
-            mbar_wait(&bars->v_full[t], 0);
-            mbar_wait(&bars->p_full[t], 0);
-            tc_fence_after();
-            issue_pv(t, 0);
-            tc_commit(&bars->o_done[t]);
-        } else {
-            mbar_wait(&bars->k_full[0], 0);
-            tc_fence_after();
-            issue_s(0);
-            tc_commit(&bars->s_full[t]);
-            tc_commit(&bars->k_empty[0]);
-            for (int j = 0; j < n_kv; ++j) {
-                const int st = j & 1;
+            tc_commit(&bars->k_empty[g % 3]);
+            if (p.packed) tc_commit(&bars->k_empty[g % 3]);  // sole consumer of this K tile
+        };
+        int gi = 0, gkv = 0;
+        for (int c = 0; c < my_items; ++c) {
+            mbar_wait(&bars->q_full, c & 1);
+            const int g0 = gkv + (p.packed ? t : 0);
+            do_s(gi, g0);
+            if (n_iter == 1) tc_commit(&bars->q_empty);
+            for (int j = 0; j < n_iter; ++j) {
                 // next scores first: S_t(j+1) only needs the softmax to have read S_t(j),
                 // so the tensor pipe computes it while P_t(j) is still being written
-                if (j + 1 < n_kv) {
-                    mbar_wait(&bars->k_full[(j + 1) % 3], ((j + 1) / 3) & 1);
-                    PAB_TRACE(lane == 0, j, t, 8);
-                    mbar_wait(&bars->s_free[t], j & 1);
-                    tc_fence_after();
-                    PAB_TRACE(lane == 0, j, t, 9);
-                    issue_s((j + 1) % 3);
-                    tc_commit(&bars->s_full[t]);
-                    tc_commit(&bars->k_empty[(j + 1) % 3]);
+                if (j + 1 < n_iter) {
+                    do_s(gi + j + 1, gkv + j + 1);
+                    if (j + 2 == n_iter) tc_commit(&bars->q_empty);  // last S of this item issued
                 }
-                mbar_wait(&bars->v_full[st], (j >> 1) & 1);
-                PAB_TRACE(lane == 0, j, t, 10);
-                mbar_wait(&bars->p_full[t], j & 1);
+                const int gv = g0 + j;
+                mbar_wait(&bars->v_full[gv & 1], (gv >> 1) & 1);
+                mbar_wait(&bars->p_full[t], (gi + j) & 1);
+                if (j == 0 && c > 0) mbar_wait(&bars->o_free[t], (c - 1) & 1);  // epilogue read O
                 tc_fence_after();
-                PAB_TRACE(lane == 0, j, t, 11);
-                issue_pv(st, j > 0);
+                issue_pv(gv & 1, j > 0);
                 tc_commit(&bars->o_done[t]);
-                PAB_TRACE(lane == 0, j, t, 12);
-                tc_commit(&bars->v_empty[st]);
+                tc_commit(&bars->v_empty[gv & 1]);
+                if (p.packed) tc_commit(&bars->v_empty[gv & 1]);
             }
+            gi += n_iter;
+            gkv += kv_per_item;
         }
     } else {
         // ================================================= softmax groups
@@ -578,131 +590,138 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int c_hi = hc ? kOChunks : (kOChunks + 1) / 2;
         const int T = p.n_k;
         const int group = p.packed ? row / T : 0;
-        const int n_iter = p.packed ? 1 : n_kv;
-        float m_run = -INFINITY, l_run = 0.f;
         const uint32_t rsw = (uint32_t)(row & 7);
-        // shared-space address of this row in the P block and its 8 swizzled 16-byte chunks
+        // shared-space address of this row in the P block
         const uint32_t p_row = smem_u32(p_blk) + (uint32_t)row * 128u;
+        const int total_iters = my_items * n_iter;
+        int gi = 0;
 
-        for (int j = 0; j < n_iter; ++j) {
-            PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 0);
-            mbar_wait(&bars->s_full[t], j & 1);
-            tc_fence_after();
-            PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 1);
-            // live score columns [lo, hi) of this row in this S tile
-            int lo = 0, hi = kKv;
-            if (p.packed) {
-                lo = group * T;
-                hi = lo + T;
-            } else if (p.n_k - j * kKv < kKv) {
-                hi = p.n_k - j * kKv;
-            }
-            // live columns of this thread's 64-column half, relative to the half
-            const int lo_c = max(lo - 64 * hc, 0), hi_c = min(hi - 64 * hc, 64);
-            const bool full = (lo_c == 0) && (hi_c == 64);
-            // ---- pass 1: this half's row max of the raw scores (scale > 0 commutes with max)
-            float mx = full ? row_max_half<true>(s_tmem, 0, 64) : row_max_half<false>(s_tmem, lo_c, hi_c);
-            // exchange with the other column half of the same rows (double-buffered slot)
-            const int slot = j & 1;
-            PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 2);
-            xch[(hc * 3 + slot) * kRows + row] = mx;
-            asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(kGroupThreads) : "memory");
-            mx = fmaxf(mx, xch[((1 - hc) * 3 + slot) * kRows + row]);
-            const float m_tile = mx * p.scale_log2;
-            PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 3);
-            // previous P.V must be finished before P smem is overwritten or O rescaled
-            if (j > 0) {
-                mbar_wait(&bars->o_done[t], (j - 1) & 1);
+        for (int c = 0; c < my_items; ++c) {
+            const Item it = decode((int)blockIdx.x + c * (int)gridDim.x);
+            float m_run = -INFINITY, l_run = 0.f;
+            for (int j = 0; j < n_iter; ++j, ++gi) {
+                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 0);
+                mbar_wait(&bars->s_full[t], gi & 1);
                 tc_fence_after();
-            }
-            // both halves see identical (m_tile, m_run) per row, so they take the same branch
-            const bool need = m_tile > m_run + 8.0f;
-            if (__any_sync(0xffffffffu, need)) {
-                const float m_new = fmaxf(m_run, m_tile);
+                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 1);
+                // live score columns [lo, hi) of this row in this S tile
+                int lo = 0, hi = kKv;
+                if (p.packed) {
+                    lo = group * T;
+                    hi = lo + T;
+                } else if (p.n_k - j * kKv < kKv) {
+                    hi = p.n_k - j * kKv;
+                }
+                // live columns of this thread's 64-column half, relative to the half
+                const int lo_c = max(lo - 64 * hc, 0), hi_c = min(hi - 64 * hc, 64);
+                const bool full = (lo_c == 0) && (hi_c == 64);
+                // ---- pass 1: this half's row max of the raw scores (scale > 0 commutes with max)
+                float mx = full ? row_max_half<true>(s_tmem, 0, 64) : row_max_half<false>(s_tmem, lo_c, hi_c);
+                // exchange with the other column half of the same rows (double-buffered slot)
+                const int slot = gi & 1;
+                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 2);
+                xch[(hc * 3 + slot) * kRows + row] = mx;
+                asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(kGroupThreads) : "memory");
+                mx = fmaxf(mx, xch[((1 - hc) * 3 + slot) * kRows + row]);
+                const float m_tile = mx * p.scale_log2;
+                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 3);
+                // previous P.V must be finished before P smem is overwritten or O rescaled
+                // (j == 0: the previous item's epilogue already waited for its last P.V)
                 if (j > 0) {
-                    const float alpha = fast_exp2(m_run - m_new);
-                    l_run *= alpha;
-                    for (int cc = c_lo; cc < c_hi; ++cc) {
-                        float o[16];
-                        PAB_TMEM_LD16(o_tmem + 16 * cc, o);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int e = 0; e < 16; ++e) o[e] *= alpha;
-                        PAB_TMEM_ST16(o_tmem + 16 * cc, o);
-                    }
-                    tmem_wait_st();
+                    mbar_wait(&bars->o_done[t], (gi - 1) & 1);
+                    tc_fence_after();
                 }
-                m_run = m_new;
-            }
-            const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
-            PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 4);
-            // ---- pass 2: P = exp2(s * scale_log2 - m) -> bf16 into this half's 128B-swizzled P block.
-            // All 64 scores are pulled from TMEM first so S can be released (s_free) and the
-            // tensor pipe can start S(j+1) while this warp is still exponentiating.
-            float v[64];
-            PAB_TMEM_LD32(s_tmem, v);
-            PAB_TMEM_LD32(s_tmem + 32, (v + 32));
-            tmem_wait_ld();
-            PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 6);
-            tc_fence_before();
-            mbar_arrive(&bars->s_free[t]);
-#ifndef PAB_NO_MUFU_TOKEN
-            // MUFU token: the two query tiles' exp2 phases strictly alternate
-            // (tile 0 of step j, tile 1 of step j, tile 0 of step j+1, ...), so one
-            // group exponentiates while the other reduces / exchanges / waits.
-            if (t == 1 || j > 0) asm volatile("bar.sync %0, %1;" ::"r"(3 + t), "r"(2 * kGroupThreads) : "memory");
-#endif
-            const float psum = full ? exp_pack_half<true>(v, p.scale_log2, neg_m, p_row, rsw, 0, 64)
-                                    : exp_pack_half<false>(v, p.scale_log2, neg_m, p_row, rsw, lo_c, hi_c);
-#ifndef PAB_NO_MUFU_TOKEN
-            if (t == 0 || j + 1 < n_iter) asm volatile("bar.arrive %0, %1;" ::"r"(4 - t), "r"(2 * kGroupThreads) : "memory");
-#endif
-            PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 7);
-            l_run += psum;
-            fence_async_smem();
-            PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 5);
-            mbar_arrive(&bars->p_full[t]);
-        }
-
-        // ------------------------------------------------------ epilogue
-        xch[(hc * 3 + 2) * kRows + row] = l_run;
-        asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(kGroupThreads) : "memory");
-        const float l_tot = l_run + xch[((1 - hc) * 3 + 2) * kRows + row];
-        mbar_wait(&bars->o_done[t], (n_iter - 1) & 1);
-        tc_fence_after();
-        bool store = false;
-        __nv_bfloat16* dst = nullptr;
-        if (p.packed) {
-            const int b = b_base(t) + group, i = row - group * T;
-            store = (group < p.packed) && (b < p.n_b) && (i < T);
-            dst = p.o + (int64_t)a_idx * p.o_sa + (int64_t)b * p.o_sb + (int64_t)i * p.o_si + (int64_t)h * p.dh;
-        } else {
-            const int i = i_base(t) + row;
-            store = i < p.n_q;
-            dst = p.o + (int64_t)a_idx * p.o_sa + (int64_t)b_base(t) * p.o_sb + (int64_t)i * p.o_si +
-                  (int64_t)h * p.dh;
-        }
-        const float inv = (l_tot > 0.f) ? 1.0f / l_tot : 0.f;
-        for (int cc = c_lo; cc < c_hi; ++cc) {
-            float o[16];
-            PAB_TMEM_LD16(o_tmem + 16 * cc, o);
-            tmem_wait_ld();
-            if (store) {
+                // both halves see identical (m_tile, m_run) per row, so they take the same branch
+                const bool need = m_tile > m_run + 8.0f;
+                if (__any_sync(0xffffffffu, need)) {
+                    const float m_new = fmaxf(m_run, m_tile);
+                    if (j > 0) {
+                        const float alpha = fast_exp2(m_run - m_new);
+                        l_run *= alpha;
+                        for (int cc = c_lo; cc < c_hi; ++cc) {
+                            float o[16];
+                            PAB_TMEM_LD16(o_tmem + 16 * cc, o);
+                            tmem_wait_ld();
 #pragma unroll
-                for (int e = 0; e < 16; e += 8) {
-                    if (16 * cc + e < p.dh) {
-                        uint32_t w[4];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            __nv_bfloat162 b2 = __floats2bfloat162_rn(o[e + 2 * q] * inv, o[e + 2 * q + 1] * inv);
-                            w[q] = *reinterpret_cast<uint32_t*>(&b2);
+                            for (int e = 0; e < 16; ++e) o[e] *= alpha;
+                            PAB_TMEM_ST16(o_tmem + 16 * cc, o);
                         }
-                        *reinterpret_cast<uint4*>(dst + 16 * cc + e) = make_uint4(w[0], w[1], w[2], w[3]);
+                        tmem_wait_st();
+                    }
+                    m_run = m_new;
+                }
+                const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
+                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 4);
+                // ---- pass 2: P = exp2(s * scale_log2 - m) -> bf16 into this half's 128B-swizzled P block.
+                // All 64 scores are pulled from TMEM first so S can be released (s_free) and the
+                // tensor pipe can start S(j+1) while this warp is still exponentiating.
+                float v[64];
+                PAB_TMEM_LD32(s_tmem, v);
+                PAB_TMEM_LD32(s_tmem + 32, (v + 32));
+                tmem_wait_ld();
+                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 6);
+                tc_fence_before();
+                mbar_arrive(&bars->s_free[t]);
+#ifndef PAB_NO_MUFU_TOKEN
+                // MUFU token: the two query tiles' exp2 phases strictly alternate
+                // (tile 0 of iteration g, tile 1 of g, tile 0 of g+1, ...), so one
+                // group exponentiates while the other reduces / exchanges / waits.
+                if (t == 1 || gi > 0) asm volatile("bar.sync %0, %1;" ::"r"(3 + t), "r"(2 * kGroupThreads) : "memory");
+#endif
+                const float psum = full ? exp_pack_half<true>(v, p.scale_log2, neg_m, p_row, rsw, 0, 64)
+                                        : exp_pack_half<false>(v, p.scale_log2, neg_m, p_row, rsw, lo_c, hi_c);
+#ifndef PAB_NO_MUFU_TOKEN
+                if (t == 0 || gi + 1 < total_iters)
+                    asm volatile("bar.arrive %0, %1;" ::"r"(4 - t), "r"(2 * kGroupThreads) : "memory");
+#endif
+                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 7);
+                l_run += psum;
+                fence_async_smem();
+                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 5);
+                mbar_arrive(&bars->p_full[t]);
+            }
+
+            // ------------------------------------------------------ epilogue of this item
+            xch[(hc * 3 + 2) * kRows + row] = l_run;
+            asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(kGroupThreads) : "memory");
+            const float l_tot = l_run + xch[((1 - hc) * 3 + 2) * kRows + row];
+            mbar_wait(&bars->o_done[t], (gi - 1) & 1);
+            tc_fence_after();
+            bool store = false;
+            __nv_bfloat16* dst = nullptr;
+            if (p.packed) {
+                const int b = b_base(it, t) + group, i = row - group * T;
+                store = (group < p.packed) && (b < p.n_b) && (i < T);
+                dst = p.o + (int64_t)it.a_idx * p.o_sa + (int64_t)b * p.o_sb + (int64_t)i * p.o_si +
+                      (int64_t)it.h * p.dh;
+            } else {
+                const int i = i_base(it, t) + row;
+                store = i < p.n_q;
+                dst = p.o + (int64_t)it.a_idx * p.o_sa + (int64_t)b_base(it, t) * p.o_sb + (int64_t)i * p.o_si +
+                      (int64_t)it.h * p.dh;
+            }
+            const float inv = (l_tot > 0.f) ? 1.0f / l_tot : 0.f;
+            for (int cc = c_lo; cc < c_hi; ++cc) {
+                float o[16];
+                PAB_TMEM_LD16(o_tmem + 16 * cc, o);
+                tmem_wait_ld();
+                if (store) {
+#pragma unroll
+                    for (int e = 0; e < 16; e += 8) {
+                        if (16 * cc + e < p.dh) {
+                            uint32_t w[4];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                w[q] = pack_bf16(o[e + 2 * q] * inv, o[e + 2 * q + 1] * inv);
+                            *reinterpret_cast<uint4*>(dst + 16 * cc + e) = make_uint4(w[0], w[1], w[2], w[3]);
+                        }
                     }
                 }
             }
+            // O may now be overwritten by the next item's first P.V
+            tc_fence_before();
+            mbar_arrive(&bars->o_free[t]);
         }
-        tc_fence_before();
     }
     __syncthreads();
     if (warp == kMmaWarp) {
@@ -775,16 +794,28 @@ int launch(const pab_attn_args* a, int packed, cudaStream_t st) {
     p.o = reinterpret_cast<__nv_bfloat16*>(a->o);
     p.o_sa = a->o_sa; p.o_sb = a->o_sb; p.o_si = a->o_si;
     p.trace = g_trace;
-    dim3 grid;
+    int64_t problems;
     if (packed) {
         p.row_tiles = (a->n_b + packed - 1) / packed;
         p.n_kv = 2;  // one KV tile per query tile
-        grid = dim3((unsigned)((p.row_tiles + 1) / 2), (unsigned)a->heads, (unsigned)a->n_a);
+        problems = a->n_a;
     } else {
         p.row_tiles = (a->n_q + kRows - 1) / kRows;
         p.n_kv = (a->n_k + kKv - 1) / kKv;
-        grid = dim3((unsigned)((p.row_tiles + 1) / 2), (unsigned)a->heads, (unsigned)((int64_t)a->n_a * a->n_b));
+        problems = (int64_t)a->n_a * a->n_b;
     }
+    p.n_pairs = (p.row_tiles + 1) / 2;
+    const int64_t items = (int64_t)p.n_pairs * a->heads * problems;
+    if (items > 0x7fffffff) return PAB_ERR_UNSUPPORTED;
+    p.n_items = (int)items;
+    static int num_sms = 0;
+    if (num_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (num_sms <= 0) num_sms = 148;
+    }
+    dim3 grid((unsigned)(p.n_items < num_sms ? p.n_items : num_sms));
     attn_tc_kernel<N128, N32><<<grid, kThreads, G::kSmem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4],
                                                                  maps[5], p);
     return launch_status("attn_tc");
