@@ -73,6 +73,22 @@ int pab_residual_modnorm_sp(const float* x_in, float* x_out,
                             int D, float eps, int mode, void* stream);
 
 /*
+ * Token-major variant used around the temporal site (kernel K2's layout):
+ * the residual stream is (n_b, n_t, n_s, D) frame-major; pending term i is
+ * read token-major (rows (b, s, t)) when bit i of pending_tm_mask is set, and
+ * h is written token-major when h_token_major != 0.  With the temporal
+ * site's QKV rows token-major, each token's T frames are contiguous rows, so
+ * temporal attention reads contiguous 128-row boxes instead of gathering
+ * frames S rows apart.  Otherwise identical to pab_residual_modnorm.
+ */
+int pab_residual_modnorm_tm(const float* x_in, float* x_out,
+                            const void* const* pending, int n_pending, uint32_t pending_tm_mask,
+                            const float* gamma, const float* beta,
+                            const float* mod, void* h_out,
+                            int64_t n_b, int64_t n_t, int64_t n_s,
+                            int D, float eps, int mode, int h_token_major, void* stream);
+
+/*
  * Fused end-of-step residual drain + classifier-free guidance + DDIM (K8).
  * Replaces: the eps combine and ddim_update of diffusion.sample
  * (pkg/src/pab_engine/diffusion.py:183-189, 100-103).

@@ -55,9 +55,13 @@ struct VecT<1> {
 // (dest = s / (n_s / n_w), t, b, s % (n_s / n_w)) so the sequence-parallel
 // frames->tokens exchange needs no pack pass.  n_w == 0: identity.
 struct RowPerm {
-    int64_t n_b, n_t, n_s, n_w;
+    int64_t n_b, n_t, n_s, n_w;  // n_w > 0: all-to-all send order; n_w == -1: token-major (b, s, t)
     __device__ __forceinline__ int64_t map(int64_t row) const {
         if (n_w == 0) return row;
+        if (n_w < 0) {
+            const int64_t s = row % n_s, bt = row / n_s, t = bt % n_t, b = bt / n_t;
+            return (b * n_s + s) * n_t + t;
+        }
         const int64_t s = row % n_s, bt = row / n_s, t = bt % n_t, b = bt / n_t;
         const int64_t sw = n_s / n_w, dst = s / sw, sl = s - dst * sw;
         return ((dst * n_t + t) * n_b + b) * sw + sl;
@@ -83,7 +87,7 @@ __global__ void __launch_bounds__(256) residual_modnorm_kernel(
             VecT<VEC>::load_f32(x_in + base + c, v[j]);
 #pragma unroll
             for (int p = 0; p < PAB_MAX_PENDING; ++p)
-                if (p < pend.n) VecT<VEC>::add_bf16(pend.p[p] + base + c, v[j]);
+                if (p < pend.n) VecT<VEC>::add_bf16(pend.p[p] + pend.src_row(p, row) * (int64_t)D + c, v[j]);
             if (write_x) VecT<VEC>::store_f32(x_out + base + c, v[j]);
         }
     }
@@ -158,7 +162,8 @@ __global__ void __launch_bounds__(256) residual_modnorm_exact_kernel(
         if (p < pend.n) {
             uint2 raw[NV];
 #pragma unroll
-            for (int j = 0; j < NV; ++j) raw[j] = __ldcs(reinterpret_cast<const uint2*>(pend.p[p] + base) + j * 32 + lane);
+            for (int j = 0; j < NV; ++j)
+                raw[j] = __ldcs(reinterpret_cast<const uint2*>(pend.p[p] + pend.src_row(p, row) * (int64_t)D) + j * 32 + lane);
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
                 const float2 a = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&raw[j].x));
@@ -342,17 +347,22 @@ __global__ void fill_uniform_kernel(void* dst, int dtype, int64_t rows, int64_t 
 
 using namespace pab;
 
+// token-major source layout of the pending terms (bit i: term i stored (b, s, t))
+struct TmState {
+    uint32_t mask;
+    int64_t t, s;
+};
 static int residual_modnorm_impl(const float* x_in, float* x_out, const void* const* pending,
                                  int n_pending, const float* gamma, const float* beta,
                                  const float* mod, void* h_out, int64_t rows, int D, float eps,
-                                 int mode, RowPerm perm, void* stream);
+                                 int mode, RowPerm perm, TmState tm, void* stream);
 
 extern "C" int pab_residual_modnorm(const float* x_in, float* x_out, const void* const* pending,
                                     int n_pending, const float* gamma, const float* beta,
                                     const float* mod, void* h_out, int64_t rows, int D, float eps,
                                     int mode, void* stream) {
     return residual_modnorm_impl(x_in, x_out, pending, n_pending, gamma, beta, mod, h_out, rows, D, eps, mode,
-                                 RowPerm{0, 0, 0, 0}, stream);
+                                 RowPerm{0, 0, 0, 0}, TmState{0u, 1, 1}, stream);
 }
 
 extern "C" int pab_residual_modnorm_sp(const float* x_in, float* x_out, const void* const* pending,
@@ -362,13 +372,26 @@ extern "C" int pab_residual_modnorm_sp(const float* x_in, float* x_out, const vo
     if (n_b < 1 || n_t < 1 || n_s < 1 || n_w < 1 || n_s % n_w != 0) return PAB_ERR_SHAPE;
     if (mode == 0) return PAB_ERR_INVALID;
     return residual_modnorm_impl(x_in, x_out, pending, n_pending, gamma, beta, mod, h_out, n_b * n_t * n_s, D,
-                                 eps, mode, RowPerm{n_b, n_t, n_s, n_w}, stream);
+                                 eps, mode, RowPerm{n_b, n_t, n_s, n_w}, TmState{0u, 1, 1}, stream);
+}
+
+extern "C" int pab_residual_modnorm_tm(const float* x_in, float* x_out, const void* const* pending,
+                                       int n_pending, uint32_t pending_tm_mask, const float* gamma,
+                                       const float* beta, const float* mod, void* h_out, int64_t n_b,
+                                       int64_t n_t, int64_t n_s, int D, float eps, int mode, int h_token_major,
+                                       void* stream) {
+    if (n_b < 1 || n_t < 1 || n_s < 1) return PAB_ERR_SHAPE;
+    if (n_pending < 0 || n_pending > PAB_MAX_PENDING) return PAB_ERR_SHAPE;
+    const int64_t rows = n_b * n_t * n_s;
+    const TmState tm{pending_tm_mask & ((1u << n_pending) - 1u), n_t, n_s};
+    return residual_modnorm_impl(x_in, x_out, pending, n_pending, gamma, beta, mod, h_out, rows, D, eps, mode,
+                                 RowPerm{n_b, n_t, n_s, h_token_major ? -1 : 0}, tm, stream);
 }
 
 static int residual_modnorm_impl(const float* x_in, float* x_out, const void* const* pending,
                                  int n_pending, const float* gamma, const float* beta,
                                  const float* mod, void* h_out, int64_t rows, int D, float eps,
-                                 int mode, RowPerm perm, void* stream) {
+                                 int mode, RowPerm perm, TmState tm, void* stream) {
     if (rows < 0 || D <= 0 || n_pending < 0 || n_pending > PAB_MAX_PENDING) return PAB_ERR_SHAPE;
     if (mode < 0 || mode > 2) return PAB_ERR_INVALID;
     if (mode == 1 && mod == nullptr) return PAB_ERR_INVALID;
@@ -376,8 +399,13 @@ static int residual_modnorm_impl(const float* x_in, float* x_out, const void* co
     if ((gamma == nullptr) != (beta == nullptr)) return PAB_ERR_INVALID;
     if (rows == 0) return PAB_OK;
     const int write_x = (n_pending > 0 || x_in != x_out) ? 1 : 0;
+    // a permuted h cannot be produced in place of a plain cast/LN row order mismatch
+    if (perm.n_w != 0 && mode == 0) return PAB_ERR_INVALID;
     if (mode == 0 && !write_x) return PAB_OK;
     PendingList pl = make_pending(pending, n_pending);
+    pl.tm_mask = tm.mask;
+    pl.tm_t = tm.t;
+    pl.tm_s = tm.s;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     auto* h = reinterpret_cast<__nv_bfloat16*>(h_out);
     bool aligned = (D % 4 == 0) && ((uintptr_t)x_in % 16 == 0) && ((uintptr_t)x_out % 16 == 0) &&

@@ -30,8 +30,19 @@ def _need(t: torch.Tensor, dtype, name: str):
         raise ValidationError(f"{name} must be {dtype}, got {t.dtype}")
 
 
-def residual_modnorm(x_in, x_out, pending, h_out=None, mod=None, gamma=None, beta=None, mode=1, eps=1e-5):
-    """x_out = x_in + sum(pending) (fp32); h_out = modnorm(x_out) (mode 1) or bf16(x_out) (mode 2)."""
+def is_token_major(t) -> bool:
+    """Site outputs of the serial temporal site are stored token-major (rows (b, s, t))."""
+    return bool(getattr(t, "pab_token_major", False))
+
+
+def residual_modnorm(x_in, x_out, pending, h_out=None, mod=None, gamma=None, beta=None, mode=1, eps=1e-5,
+                     shape=None, h_token_major=False):
+    """x_out = x_in + sum(pending) (fp32); h_out = modnorm(x_out) (mode 1) or bf16(x_out) (mode 2).
+
+    ``shape`` = (B, T, S) of the residual stream; needed when a pending term is
+    token-major (``is_token_major``) or when ``h_token_major`` asks for h in
+    (b, s, t) row order (the temporal site's input layout).
+    """
     lib = _lib.load()
     _need(x_in, torch.float32, "x_in")
     _need(x_out, torch.float32, "x_out")
@@ -47,30 +58,33 @@ def residual_modnorm(x_in, x_out, pending, h_out=None, mod=None, gamma=None, bet
         _need(h_out, torch.bfloat16, "h_out")
         if h_out.numel() != x_in.numel():
             raise ShapeError("h_out does not match the residual stream")
+    tm_needed = h_token_major or any(is_token_major(p) for p in pending)
+    if tm_needed:
+        if shape is None or shape[0] * shape[1] * shape[2] != rows:
+            raise ShapeError("token-major residual terms need the (B, T, S) shape of the stream")
     pend = list(pending)
     src = x_in
+
+    def call(terms, h, m, md, tokmaj):
+        arr = _lib.ptr_array([p.data_ptr() for p in terms])
+        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        if tm_needed:
+            mask = sum(1 << i for i, p in enumerate(terms) if is_token_major(p))
+            st = lib.pab_residual_modnorm_tm(src.data_ptr(), x_out.data_ptr(), arr, len(terms), mask, ptr(gamma),
+                                             ptr(beta), ptr(md), ptr(h), shape[0], shape[1], shape[2], D,
+                                             float(eps), int(m), int(tokmaj), _stream())
+            _lib.check(st, "pab_residual_modnorm_tm")
+        else:
+            st = lib.pab_residual_modnorm(src.data_ptr(), x_out.data_ptr(), arr, len(terms), ptr(gamma), ptr(beta),
+                                          ptr(md), ptr(h), rows, D, float(eps), int(m), _stream())
+            _lib.check(st, "pab_residual_modnorm")
+
     # more than MAX_PENDING terms: drain in order, normalising only on the last chunk
     while len(pend) > MAX_PENDING:
         chunk, pend = pend[:MAX_PENDING], pend[MAX_PENDING:]
-        arr = _lib.ptr_array([p.data_ptr() for p in chunk])
-        _lib.check(
-            lib.pab_residual_modnorm(src.data_ptr(), x_out.data_ptr(), arr, len(chunk), None, None, None, None,
-                                     rows, D, eps, 0, _stream()),
-            "pab_residual_modnorm",
-        )
+        call(chunk, None, 0, None, False)
         src = x_out
-    arr = _lib.ptr_array([p.data_ptr() for p in pend])
-    _lib.check(
-        lib.pab_residual_modnorm(
-            src.data_ptr(), x_out.data_ptr(), arr, len(pend),
-            gamma.data_ptr() if gamma is not None else None,
-            beta.data_ptr() if beta is not None else None,
-            mod.data_ptr() if mod is not None else None,
-            h_out.data_ptr() if h_out is not None else None,
-            rows, D, float(eps), int(mode), _stream(),
-        ),
-        "pab_residual_modnorm",
-    )
+    call(pend, h_out, mode, mod, h_token_major)
 
 
 def residual_modnorm_sp(x_in, x_out, pending, h_out, shard_shape, n_w, mod=None, gamma=None, beta=None, mode=1,
@@ -113,9 +127,8 @@ def ddim_cfg(z, r, pending, guidance: bool, guidance_scale: float, a_cur: float,
     batch = z.shape[0]
     n = z.numel() // batch
     pend = list(pending)
-    while len(pend) > MAX_PENDING:  # fold excess terms into r first (same add order)
-        residual_modnorm(r, r, pend[:MAX_PENDING], mode=0)
-        pend = pend[MAX_PENDING:]
+    if any(is_token_major(p) for p in pend) or len(pend) > MAX_PENDING:
+        raise ShapeError("ddim_cfg takes at most MAX_PENDING frame-major terms; flush the rest first")
     arr = _lib.ptr_array([p.data_ptr() for p in pend])
     _lib.check(
         lib.pab_ddim_cfg(z.data_ptr(), r.data_ptr(), arr, len(pend), batch, n, int(bool(guidance)),

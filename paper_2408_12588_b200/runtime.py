@@ -95,6 +95,10 @@ class StepContext:
         self.qbuf = torch.empty((rows, D), **bf)
         self.zero_bias = torch.zeros((self.R,), **bf)
         self.o_scratch = torch.empty((rows, D), **bf)
+        # the serial temporal site works token-major (rows (b, s, t)); its outputs carry a marker
+        self.o_scratch_tm = torch.empty((rows, D), **bf)
+        self.o_scratch_tm.pab_token_major = True
+        self.shape3 = (batch, self.T, self.S)
         self.launches = Launches()
         # debugging override (the default, "auto", selects the tcgen05 kernel for every model shape)
         self.attn_impl = {"auto": kernels.IMPL_AUTO, "tcgen05": kernels.IMPL_TCGEN05,
@@ -125,10 +129,11 @@ class StepContext:
         self.args_spatial = kernels.attn_args(
             q, k, v, self.attn_out, (S * ld, 0, ld), (S * ld, 0, ld), (S * ld, 0, ld), (S * D, 0, D),
             B * T, 1, S, S, H, dh)
-        # temporal: problem (a = batch, b = token), rows = frames (stride S rows)
+        # temporal: token-major rows (b, s, t) written by the prologue, so each
+        # problem (b, s) is T contiguous rows; problems are consecutive (stride T rows)
         self.args_temporal = kernels.attn_args(
-            q, k, v, self.attn_out, (T * S * ld, ld, S * ld), (T * S * ld, ld, S * ld), (T * S * ld, ld, S * ld),
-            (T * S * D, D, S * D), B, S, T, T, H, dh)
+            q, k, v, self.attn_out, (0, T * ld, ld), (0, T * ld, ld), (0, T * ld, ld), (0, T * D, D),
+            1, B * S, T, T, H, dh)
         # cross: q rows = all (frame, token) of a batch entry, keys = text tokens
         self.args_cross = []
         for kv_s, kv_t in self.text_kv:
@@ -188,13 +193,14 @@ class _Step:
         self.mods = ctx.mods[step]
 
     # -- helpers ---------------------------------------------------------
-    def prologue(self, mode: int, mod=None, ln=None):
+    def prologue(self, mode: int, mod=None, ln=None, token_major=False):
         c = self.ctx
         gamma = beta = None
         if ln is not None and not c.params.ln_identity:
             gamma, beta = ln
         kernels.residual_modnorm(self.src.view(-1, c.D), self.r.view(-1, c.D), self.pending, h_out=c.h,
-                                 mod=mod, gamma=gamma, beta=beta, mode=mode)
+                                 mod=mod, gamma=gamma, beta=beta, mode=mode, shape=c.shape3,
+                                 h_token_major=token_major)
         c.launches.prologue_calls += 1
         self.src = self.r
         self.pending = []
@@ -203,14 +209,20 @@ class _Step:
         """Materialise the residual stream (no normalised output)."""
         c = self.ctx
         if self.pending or self.src is not self.r:
-            kernels.residual_modnorm(self.src.view(-1, c.D), self.r.view(-1, c.D), self.pending, mode=0)
+            kernels.residual_modnorm(self.src.view(-1, c.D), self.r.view(-1, c.D), self.pending, mode=0,
+                                     shape=c.shape3)
             c.launches.prologue_calls += 1
         self.src = self.r
         self.pending = []
 
-    def out_buffer(self, store: bool):
+    def out_buffer(self, store: bool, token_major: bool = False):
         c = self.ctx
-        return torch.empty((c.rows, c.D), device=c.h.device, dtype=torch.bfloat16) if store else c.o_scratch
+        if not store:
+            return c.o_scratch_tm if token_major else c.o_scratch
+        o = torch.empty((c.rows, c.D), device=c.h.device, dtype=torch.bfloat16)
+        if token_major:
+            o.pab_token_major = True
+        return o
 
     def record(self, li, kind, block, decision, source, o):
         c = self.ctx
@@ -219,14 +231,14 @@ class _Step:
             self.trace.observe(TraceRecord(step=self.step, timestep=self.t, layer=li, kind=kind, block=block,
                                            decision=decision, source_step=source), o)
 
-    def run_site(self, li, kind, block, compute):
+    def run_site(self, li, kind, block, compute, token_major=False):
         d = self.decisions
         source = d.source(li, kind)
         site = (li, kind, block)
         c = self.ctx
         if source == self.step:
             store = d.should_store(li, kind)
-            o = compute(self.out_buffer(store))
+            o = compute(self.out_buffer(store, token_major))
             if store:
                 self.cache.store(site, o, self.step, "outputs")
             self.sink.site(kind, block)
@@ -247,7 +259,7 @@ class _Step:
         c = self.ctx
 
         def compute(o):
-            self.prologue(1, self.mods[self._li, slot], (p.ln_gamma, p.ln_beta))
+            self.prologue(1, self.mods[self._li, slot], (p.ln_gamma, p.ln_beta), token_major=temporal)
             torch.mm(c.h, p.w_qkv, out=c.qkv)
             kernels.attention(c.args_temporal if temporal else c.args_spatial, c.attn_impl)
             torch.mm(c.attn_out, p.wo, out=o)
@@ -311,7 +323,7 @@ class _Step:
         if temporal_hook is not None:
             temporal_hook(self, li, lp)
         else:
-            self.run_site(li, TM, "t", self.attn_site(lp.temporal, MOD_TEMPORAL, True))
+            self.run_site(li, TM, "t", self.attn_site(lp.temporal, MOD_TEMPORAL, True), token_major=True)
         if self.ctx.cfg.cross_in_temporal:
             self.run_site(li, CR, "t", self.cross_site(lp.cross_temporal, 1))
         self.run_site(li, ML, "t", self.mlp_site(lp.mlp_temporal, MOD_MLP_T))
@@ -333,11 +345,21 @@ def run_forward(ctx: StepContext, step_index: int, t: float, z, r, decisions, ca
         st.flush()
     else:
         guidance, g, a_cur, a_next = ddim
-        if st.src is not st.r:  # nothing ran (L == 0 cannot happen, but stay exact)
-            st.flush()
+        if st.src is not st.r or len(st.pending) > kernels.MAX_PENDING or any(
+                kernels.is_token_major(p) for p in st.pending):
+            st.flush()  # the fused DDIM kernel drains frame-major terms only
         kernels.ddim_cfg(z, st.r, st.pending, guidance, g, a_cur, a_next)
         ctx.launches.other_calls += 1
     return time.perf_counter() - t0
 
 
-__all__ = ["StepContext", "run_forward", "Launches", "ATTENTION_KINDS"]
+def canonical(o, shape):
+    """Frame-major (B, T, S, D) view of a site output (token-major outputs of the
+    serial temporal site are permuted back); for tests and gathered caches."""
+    B, T, S = shape
+    if kernels.is_token_major(o):
+        return o.view(B, S, T, -1).permute(0, 2, 1, 3).reshape(B, T, S, -1)
+    return o.view(B, T, S, -1)
+
+
+__all__ = ["StepContext", "run_forward", "Launches", "ATTENTION_KINDS", "canonical"]

@@ -31,8 +31,9 @@ ld = 3 * D
 q, k, v = qkv[:, :D], qkv[:, D:2 * D], qkv[:, 2 * D:]
 sp = kernels.attn_args(q, k, v, out, (S * ld, 0, ld), (S * ld, 0, ld), (S * ld, 0, ld), (S * D, 0, D), B * T, 1, S, S,
                        H, dh)
-st = (T * S * ld, ld, S * ld)
-tm = kernels.attn_args(q, k, v, out, st, st, st, (T * S * D, D, S * D), B, S, T, T, H, dh)
+# temporal site layout used by the engine: token-major rows (b, s, t)
+st = (0, T * ld, ld)
+tm = kernels.attn_args(q, k, v, out, st, st, st, (0, T * D, D), 1, B * S, T, T, H, dh)
 cr = kernels.attn_args(q, kv[:, :D], kv[:, D:], out, (T * S * ld, 0, ld), (M * 2 * D, 0, 2 * D),
                        (M * 2 * D, 0, 2 * D), (T * S * D, 0, D), B, 1, T * S, M, H, dh)
 peaks, _ = load_peaks()

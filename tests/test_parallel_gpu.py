@@ -56,8 +56,12 @@ def _worker(rank, world, port, guidance, q):
             model = comm_volume_model("broadcast_sp", cfg, sched, table, world, batch=2 if guidance else 1)
             out["ledger_ok"] = par.comm_report.grouped_elements() == model.grouped_elements()
             worst = 0.0
+            from paper_2408_12588_b200.runtime import canonical
+
+            B = 2 if guidance else 1
             for site, val in gathered.items():
-                ref = ser.cache.entries[site].value.float().cpu().numpy().reshape(val.shape)
+                ref = canonical(ser.cache.entries[site].value, (B, cfg.frames, cfg.spatial_tokens))
+                ref = ref.float().cpu().numpy().reshape(val.shape)
                 worst = max(worst, float(np.linalg.norm(val - ref) / max(np.linalg.norm(ref), 1e-12)))
             out["cache_rel"] = worst
             out["n_cache"] = len(gathered)
