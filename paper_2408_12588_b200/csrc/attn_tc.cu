@@ -274,22 +274,29 @@ template <bool FULL>
 __device__ __forceinline__ float exp_pack_half(const float* v, float scale_log2, float neg_m, uint32_t p_row,
                                                uint32_t rsw, int lo_c, int hi_c) {
     if (FULL) {
+        // x = s * scale_log2 - m for all 64 scores (FFMA2), then all exp2 back to back so
+        // the MUFU queue stays full, then row sum (FADD2) + bf16 pack + swizzled stores
+        float e[64];
         const unsigned long long sc2 = f2_pack(scale_log2, scale_log2), nm2 = f2_pack(neg_m, neg_m);
+#pragma unroll
+        for (int c = 0; c < 64; c += 2) {
+            const float2 x = f2_unpack(f2_fma(f2_pack(v[c], v[c + 1]), sc2, nm2));
+            e[c] = x.x;
+            e[c + 1] = x.y;
+        }
+#pragma unroll
+        for (int c = 0; c < 64; ++c)
+            // optionally every PAB_POLY_EVERY-th score on the FMA pipe (polynomial exp2)
+            e[c] = (PAB_POLY_EVERY > 0 && (c % PAB_POLY_DIV) == PAB_POLY_DIV - 1) ? poly_exp2(e[c]) : fast_exp2(e[c]);
         unsigned long long acc2[2] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            float e[8];
 #pragma unroll
-            for (int c = 0; c < 8; c += 2) {
-                const float2 x = f2_unpack(f2_fma(f2_pack(v[8 * k + c], v[8 * k + c + 1]), sc2, nm2));
-                e[c] = fast_exp2(x.x);
-                // optionally every PAB_POLY_EVERY-th score on the FMA pipe (polynomial exp2)
-                e[c + 1] = (PAB_POLY_EVERY > 0 && ((c + 1) % PAB_POLY_DIV) == PAB_POLY_DIV - 1) ? poly_exp2(x.y)
-                                                                                               : fast_exp2(x.y);
-                acc2[(c >> 1) & 1] = f2_add(acc2[(c >> 1) & 1], f2_pack(e[c], e[c + 1]));
-            }
-            st_shared_v4(p_row + ((((uint32_t)k) ^ rsw) << 4), pack_bf16(e[0], e[1]), pack_bf16(e[2], e[3]),
-                         pack_bf16(e[4], e[5]), pack_bf16(e[6], e[7]));
+            for (int c = 0; c < 8; c += 2)
+                acc2[(c >> 1) & 1] = f2_add(acc2[(c >> 1) & 1], f2_pack(e[8 * k + c], e[8 * k + c + 1]));
+            st_shared_v4(p_row + ((((uint32_t)k) ^ rsw) << 4), pack_bf16(e[8 * k], e[8 * k + 1]),
+                         pack_bf16(e[8 * k + 2], e[8 * k + 3]), pack_bf16(e[8 * k + 4], e[8 * k + 5]),
+                         pack_bf16(e[8 * k + 6], e[8 * k + 7]));
         }
         const float2 a0 = f2_unpack(acc2[0]), a1 = f2_unpack(acc2[1]);
         return (a0.x + a0.y) + (a1.x + a1.y);
@@ -493,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == kMmaWarp || warp == kMmaWarp + 1) {
         // ============================ MMA issuer of query tile t (warp-wide, elected lane issues)
         const int t = warp - kMmaWarp;
-        constexpr uint32_t idS = idesc_bf16(128, 128, 0);
+        constexpr uint32_t idS128 = idesc_bf16(128, 128, 0);
         constexpr uint32_t idO = idesc_bf16(128, G::kDhPad, 1);
         const uint32_t q_addr = smem_u32(smem + G::kQ0 + t * G::kTileBytes);
         const uint32_t k_addr = smem_u32(smem + G::kK0);
@@ -510,8 +517,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // V: MN-major SW32, 16-column atoms 4096 B apart (LBO), 8-row groups 256 B apart (SBO)
         const uint64_t dv = smem_desc(v_addr, 4096, 256, kLayoutSW32);
         // S_t = Q_t K^T over the dh K-blocks (K-major operands)
-        auto issue_s = [&](int st) {
+        // ncols: key columns of this S tile rounded up to 16 (a partial last tile runs N < 128)
+        auto issue_s = [&](int st, int ncols) {
             const uint32_t ko = (st * G::kTileBytes) >> 4;
+            const uint32_t idS = (idS128 & ~(0x3Fu << 17)) | ((uint32_t)(ncols >> 3) << 17);
             uint32_t acc = 0;
 #pragma unroll
             for (int blk = 0; blk < N128; ++blk)
@@ -528,20 +537,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc = 1;
             }
         };
-        // O_t += P_t V: 8 K-steps of 16 keys, each one N = kDhPad MMA
-        auto issue_pv = [&](int st, uint32_t accumulate) {
+        // O_t += P_t V: ncols / 16 K-steps of 16 keys, each one N = kDhPad MMA
+        auto issue_pv = [&](int st, uint32_t accumulate, int ncols) {
             const uint32_t vo = (st * G::kTileBytes) >> 4;
 #pragma unroll
             for (int k = 0; k < kKv / 16; ++k)
-                tc_mma(d_o, dp + (((k >> 2) * 16384 + 32 * (k & 3)) >> 4), dv + vo + ((512 * k) >> 4), idO,
-                       (accumulate || k > 0) ? 1u : 0u);
+                if (16 * k < ncols)
+                    tc_mma(d_o, dp + (((k >> 2) * 16384 + 32 * (k & 3)) >> 4), dv + vo + ((512 * k) >> 4), idO,
+                           (accumulate || k > 0) ? 1u : 0u);
+        };
+        auto cols_of = [&](int j) {
+            if (p.packed) return kKv;
+            const int n = min(kKv, p.n_k - j * kKv);
+            return (n + 15) & ~15;
         };
         // S for global iteration gi from K ring slot g; the softmax must have released S(gi - 1)
-        auto do_s = [&](int gi, int g) {
+        auto do_s = [&](int gi, int g, int ncols) {
             mbar_wait(&bars->k_full[g % 3], (g / 3) & 1);
             if (gi > 0) mbar_wait(&bars->s_free[t], (gi - 1) & 1);
             tc_fence_after();
-            issue_s(g % 3);
+            issue_s(g % 3, ncols);
             tc_commit(&bars->s_full[t]);
             tc_commit(&bars->k_empty[g % 3]);
             if (p.packed) tc_commit(&bars->k_empty[g % 3]);  // sole consumer of this K tile
@@ -550,13 +565,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < my_items; ++c) {
             mbar_wait(&bars->q_full, c & 1);
             const int g0 = gkv + (p.packed ? t : 0);
-            do_s(gi, g0);
+            do_s(gi, g0, cols_of(0));
             if (n_iter == 1) tc_commit(&bars->q_empty);
             for (int j = 0; j < n_iter; ++j) {
                 // next scores first: S_t(j+1) only needs the softmax to have read S_t(j),
                 // so the tensor pipe computes it while P_t(j) is still being written
                 if (j + 1 < n_iter) {
-                    do_s(gi + j + 1, gkv + j + 1);
+                    do_s(gi + j + 1, gkv + j + 1, cols_of(j + 1));
                     if (j + 2 == n_iter) tc_commit(&bars->q_empty);  // last S of this item issued
                 }
                 const int gv = g0 + j;
@@ -564,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&bars->p_full[t], (gi + j) & 1);
                 if (j == 0 && c > 0) mbar_wait(&bars->o_free[t], (c - 1) & 1);  // epilogue read O
                 tc_fence_after();
-                issue_pv(gv & 1, j > 0);
+                issue_pv(gv & 1, j > 0, cols_of(j));
                 tc_commit(&bars->o_done[t]);
                 tc_commit(&bars->v_empty[gv & 1]);
                 if (p.packed) tc_commit(&bars->v_empty[gv & 1]);
@@ -616,7 +631,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int lo_c = max(lo - 64 * hc, 0), hi_c = min(hi - 64 * hc, 64);
                 const bool full = (lo_c == 0) && (hi_c == 64);
                 // ---- pass 1: this half's row max of the raw scores (scale > 0 commutes with max)
-                float mx = full ? row_max_half<true>(s_tmem, 0, 64) : row_max_half<false>(s_tmem, lo_c, hi_c);
+                // false: this half lies past a partial last tile, whose P.V does not read it
+                // (packed tiles always run the masked path: their P.V reads all 128 keys)
+                const bool live = p.packed || hi_c > lo_c;
+                float mx = full   ? row_max_half<true>(s_tmem, 0, 64)
+                           : live ? row_max_half<false>(s_tmem, lo_c, hi_c)
+                                  : -INFINITY;
                 // exchange with the other column half of the same rows (double-buffered slot)
                 const int slot = gi & 1;
                 PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 2);
@@ -655,6 +675,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // ---- pass 2: P = exp2(s * scale_log2 - m) -> bf16 into this half's 128B-swizzled P block.
                 // All 64 scores are pulled from TMEM first so S can be released (s_free) and the
                 // tensor pipe can start S(j+1) while this warp is still exponentiating.
+                // (a half past a partial last tile loads stale columns it never uses)
                 float v[64];
                 PAB_TMEM_LD32(s_tmem, v);
                 PAB_TMEM_LD32(s_tmem + 32, (v + 32));
@@ -668,8 +689,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // group exponentiates while the other reduces / exchanges / waits.
                 if (t == 1 || gi > 0) asm volatile("bar.sync %0, %1;" ::"r"(3 + t), "r"(2 * kGroupThreads) : "memory");
 #endif
-                const float psum = full ? exp_pack_half<true>(v, p.scale_log2, neg_m, p_row, rsw, 0, 64)
-                                        : exp_pack_half<false>(v, p.scale_log2, neg_m, p_row, rsw, lo_c, hi_c);
+                const float psum = full   ? exp_pack_half<true>(v, p.scale_log2, neg_m, p_row, rsw, 0, 64)
+                                   : live ? exp_pack_half<false>(v, p.scale_log2, neg_m, p_row, rsw, lo_c, hi_c)
+                                          : 0.f;  // the P.V of this tile does not read this half
 #ifndef PAB_NO_MUFU_TOKEN
                 if (t == 0 || gi + 1 < total_iters)
                     asm volatile("bar.arrive %0, %1;" ::"r"(4 - t), "r"(2 * kGroupThreads) : "memory");
