@@ -228,9 +228,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("PAB_DIST_BACKEND", "nccl") != "nccl":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL over NVLink in production; PAB_DIST_BACKEND=gloo lets several ranks share one
+        # GPU to exercise this multi-rank path where only one GPU is available
+        backend = os.environ.get("PAB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     cfg = model_config(c)
     params = init_model(cfg, seed=11)
     sched = make_schedule(c["steps"])
