@@ -130,7 +130,9 @@ int pab_fill_uniform(void* dst, int dtype, int64_t rows, int64_t cols, int64_t l
  *   cross   : a = batch, i = (frame, token) for q/o, i = text token for k/v
  * Output o uses the same addressing with (o_sa, o_sb, o_si).
  * impl: 0 = auto (tcgen05/TMA kernel when the shape allows), 1 = force the
- * tcgen05 kernel (error if unsupported), 2 = force the SIMT kernel.
+ * tcgen05 kernels (row-per-thread kernel for long sequences, block-diagonal
+ * packed kernel for short ones; error if unsupported), 2 = force the SIMT
+ * kernel, 3 = the earlier split-row tcgen05 kernel for every shape (A/B only).
  */
 typedef struct {
     const void* q; const void* k; const void* v; void* o;

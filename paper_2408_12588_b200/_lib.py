@@ -13,7 +13,8 @@ import os
 from .errors import DeviceError, raise_for_status
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpab_b200.so")
+# PAB_LIB_PATH: load a differently-built copy (kernel A/B experiments, scripts/gpu_variants.sh)
+LIB_PATH = os.environ.get("PAB_LIB_PATH") or os.path.join(_HERE, "libpab_b200.so")
 MAX_PENDING = 8
 
 _lib = None

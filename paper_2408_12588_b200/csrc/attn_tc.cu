@@ -26,6 +26,7 @@
 // softmax masks the block diagonal, so the short problems still run on
 // 128x128 tensor-core tiles; the kernel is HBM-bound there.
 #include "common.cuh"
+#include "tc_ptx.cuh"
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <math.h>
@@ -71,151 +72,6 @@ struct Params {
     } while (0)
 #endif
 
-// ---------------------------------------------------------------- PTX wrappers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    // try_wait with a suspend-time hint: the warp sleeps in hardware until the
-    // phase completes (or the hint expires) instead of spinning on issue slots
-    const uint32_t addr = smem_u32(bar);
-    asm volatile(
-        "{\n\t.reg .pred done;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, %2;\n\t"
-        "@!done bra WAIT_%=;\n}" ::"r"(addr),
-        "r"(parity), "r"(0x989680)
-        : "memory");
-}
-// producer-side wait with a nanosleep backoff so a far-ahead TMA lane does not
-// steal issue slots from the softmax warps sharing its SM sub-partition
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-    const uint32_t addr = smem_u32(bar);
-    uint32_t done = 0;
-    while (true) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(addr), "r"(parity)
-            : "memory");
-        if (done) break;
-        __nanosleep(256);
-    }
-}
-__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-#ifdef PAB_STS_VOLATILE
-    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-#else
-    // no memory clobber: lets the scheduler overlap the exp2 of the next chunk with
-    // this store (ordering w.r.t. the tensor core comes from fence.proxy.async + mbarrier)
-    asm("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d));
-#endif
-}
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-    __nv_bfloat162 b2 = __floats2bfloat162_rn(lo, hi);
-    return *reinterpret_cast<uint32_t*>(&b2);
-}
-
-__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                            int c2, int c3, int c4) {
-    asm volatile(
-        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
-        : "memory");
-}
-__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// tcgen05.mma / commit are issued by one elected lane of a warp that runs the
-// issue loop warp-wide, so descriptors stay in uniform registers
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-    asm volatile(
-        "{\n\t.reg .pred e;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                       uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-
-#define PAB_TMEM_LD32(taddr, r)                                                                              \
-    asm volatile(                                                                                            \
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"    \
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                           \
-        : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7]),    \
-          "=f"(r[8]), "=f"(r[9]), "=f"(r[10]), "=f"(r[11]), "=f"(r[12]), "=f"(r[13]), "=f"(r[14]),          \
-          "=f"(r[15]), "=f"(r[16]), "=f"(r[17]), "=f"(r[18]), "=f"(r[19]), "=f"(r[20]), "=f"(r[21]),        \
-          "=f"(r[22]), "=f"(r[23]), "=f"(r[24]), "=f"(r[25]), "=f"(r[26]), "=f"(r[27]), "=f"(r[28]),        \
-          "=f"(r[29]), "=f"(r[30]), "=f"(r[31])                                                              \
-        : "r"(taddr))
-
-#define PAB_TMEM_LD16(taddr, r)                                                                              \
-    asm volatile(                                                                                            \
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"   \
-        " [%16];"                                                                                            \
-        : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7]),    \
-          "=f"(r[8]), "=f"(r[9]), "=f"(r[10]), "=f"(r[11]), "=f"(r[12]), "=f"(r[13]), "=f"(r[14]),          \
-          "=f"(r[15])                                                                                        \
-        : "r"(taddr))
-
-#define PAB_TMEM_ST16(taddr, r)                                                                              \
-    asm volatile(                                                                                            \
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15," \
-        "%16};" ::"r"(taddr),                                                                                \
-        "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7]), "f"(r[8]),   \
-        "f"(r[9]), "f"(r[10]), "f"(r[11]), "f"(r[12]), "f"(r[13]), "f"(r[14]), "f"(r[15])                    \
-        : "memory")
-
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-__device__ __forceinline__ float fast_exp2(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
-// exp2 on the FMA/ALU pipes only (no FRND/F2I, which share the XU pipe with
-// MUFU.EX2): round-to-nearest via the 1.5*2^23 magic constant, then a degree-4
-// Taylor polynomial of 2^f on [-0.5, 0.5] (rel err < 5e-5, far below the bf16
-// rounding of P).  Used for a share of the scores so MUFU is not the only exp2
-// engine.  Inputs are clamped at -127 (x -> -inf gives ~0).
-__device__ __forceinline__ float poly_exp2(float x) {
-    x = fmaxf(x, -127.0f);
-    const float t = x + 12582912.0f;                 // 1.5 * 2^23: integer part lands in the low mantissa
-    const int xi = __float_as_int(t) - 0x4B400000;   // round(x)
-    const float f = x - (t - 12582912.0f);           // x - round(x) in [-0.5, 0.5]
-    float pf = fmaf(f, 0.009618129f, 0.05550411f);
-    pf = fmaf(pf, f, 0.2402265f);
-    pf = fmaf(pf, f, 0.6931472f);
-    pf = fmaf(pf, f, 1.0f);
-    return __int_as_float(__float_as_int(pf) + (xi << 23));
-}
 
 #ifndef PAB_POLY_EVERY
 #define PAB_POLY_EVERY 8
@@ -245,28 +101,6 @@ __device__ __forceinline__ float row_max_half(uint32_t s_tmem, int lo_c, int hi_
     return mx;
 }
 
-// packed fp32x2 helpers (Blackwell FFMA2 / FADD2: two lanes of work per issue slot)
-__device__ __forceinline__ unsigned long long f2_pack(float a, float b) {
-    unsigned long long r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ float2 f2_unpack(unsigned long long r) {
-    float2 v;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
-    return v;
-}
-__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b,
-                                                     unsigned long long c) {
-    unsigned long long r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-    return r;
-}
-__device__ __forceinline__ unsigned long long f2_add(unsigned long long a, unsigned long long b) {
-    unsigned long long r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
 
 // P = exp2(s * scale_log2 - m) for this thread's 64 scores -> bf16 into its 128-byte
 // swizzled P row; returns the row-sum contribution.
@@ -317,26 +151,6 @@ __device__ __forceinline__ float exp_pack_half(const float* v, float scale_log2,
     return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
-// ------------------------------------------------------ UMMA descriptors
-// Shared-memory matrix descriptor (sm_100): start>>4 [0,14), LBO>>4 [16,30),
-// SBO>>4 [32,46), version=1 [46,48), base offset [49,52), layout [61,64).
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
-    uint64_t d = 0;
-    d |= (uint64_t)((addr >> 4) & 0x3FFF);
-    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-    d |= (uint64_t)1 << 46;
-    d |= (uint64_t)layout << 61;
-    return d;
-}
-constexpr uint32_t kLayoutSW128 = 2, kLayoutSW32 = 6;
-
-// Instruction descriptor, kind::f16: D=f32 [4,6)=1, A=bf16 [7,10)=1, B=bf16 [10,13)=1,
-// A major [15], B major [16] (0 = K-major, 1 = MN-major), N>>3 [17,23), M>>4 [24,29).
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int b_mn_major) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) |
-           ((uint32_t)(M >> 4) << 24);
-}
 
 // ------------------------------------------------------------- the kernel
 template <int N128, int N32>
@@ -868,6 +682,8 @@ bool attn_tc_supported(const pab_attn_args* a) {
     if (a->n_a > 0x7fffffff || a->n_q > (1 << 30)) return false;
     return tc::get_encode() != nullptr;
 }
+
+int attn_tc_packing(const pab_attn_args* a) { return tc::packing_for(a); }
 
 int attn_tc_launch(const pab_attn_args* a, cudaStream_t st) {
     const int packed = tc::packing_for(a);

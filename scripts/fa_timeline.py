@@ -1,0 +1,41 @@
+"""Print the clock64 event timeline of CTA 0 of the row-per-thread attention kernel
+(library built with -DPAB_FA_TRACE, e.g. scripts/build_variant.sh trace -DPAB_FA_TRACE)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2408_12588_b200 import _lib, kernels  # noqa: E402
+
+B, T, S, D, H = 2, 16, 1560, 1152, 16
+dh = D // H
+rows = B * T * S
+qkv = torch.randn(rows, 3 * D, device="cuda").to(torch.bfloat16)
+out = torch.empty(rows, D, device="cuda", dtype=torch.bfloat16)
+ld = 3 * D
+a = kernels.attn_args(qkv[:, :D], qkv[:, D:2 * D], qkv[:, 2 * D:], out, (S * ld, 0, ld), (S * ld, 0, ld),
+                      (S * ld, 0, ld), (S * D, 0, D), B * T, 1, S, S, H, dh)
+buf = torch.zeros(64 * 2 * 16, dtype=torch.int64, device="cuda")
+lib = _lib.load()
+for _ in range(3):
+    kernels.attention(a)
+lib.pab_attn_debug_trace(buf.data_ptr())
+kernels.attention(a)
+torch.cuda.synchronize()
+lib.pab_attn_debug_trace(None)
+tr = buf.view(64, 2, 16).cpu()
+t0 = int(tr[tr > 0].min())
+names = {0: "sm:wait_S", 1: "sm:S_ready", 2: "sm:S_loaded", 3: "sm:max_done", 4: "sm:P_stored", 5: "sm:p_full",
+         10: "mma:wait_P", 8: "mma:P_ok", 9: "mma:PV+S_issued"}
+ev = []
+for j in range(int(os.environ.get("TL_ITERS", "30"))):
+    for t in range(2):
+        for e, nm in names.items():
+            v = int(tr[j, t, e])
+            if v:
+                ev.append((v - t0, j, t, nm))
+prev = 0
+for v, j, t, nm in sorted(ev):
+    print(f"{v:8d} (+{v - prev:5d})  it={j:2d} t={t}  {nm}")
+    prev = v

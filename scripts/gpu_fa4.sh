@@ -1,0 +1,3 @@
+timeout -s KILL 600 python -m pytest tests/test_kernels_gpu.py -q -m gpu -x -k "attention and not tc_split" > gpurun_out/t_attn.log 2>&1; echo "attn tests rc=$?"; tail -2 gpurun_out/t_attn.log
+timeout -s KILL 120 python scripts/bench_attn.py --config C3 --impl 1
+echo "== trace"; PAB_LIB_PATH=$PWD/_variants/trace.so TL_ITERS=8 timeout -s KILL 120 python scripts/fa_timeline.py | tail -40

@@ -78,19 +78,42 @@ def cross_case(B, N, M, H, dh, impl, seed=2):
     return out, want, a
 
 
-IMPLS = [kernels.IMPL_TCGEN05, kernels.IMPL_SIMT]
+IMPLS = [kernels.IMPL_TCGEN05, kernels.IMPL_SIMT, kernels.IMPL_TC_SPLIT]
+IMPL_IDS = ["tcgen05", "simt", "tc_split"]
 
 
-@pytest.mark.parametrize("impl", IMPLS, ids=["tcgen05", "simt"])
+@pytest.mark.parametrize("impl", IMPLS, ids=IMPL_IDS)
 @pytest.mark.parametrize("B,T,S,H,dh", [(1, 2, 1024, 2, 72), (1, 1, 1560, 2, 72), (2, 1, 200, 3, 72),
                                          (1, 2, 16, 4, 8), (1, 1, 300, 2, 16), (1, 1, 129, 1, 64),
-                                         (1, 1, 77, 2, 32)])
+                                         (1, 1, 77, 2, 32), (1, 1, 100, 2, 56), (1, 8, 1024, 16, 72),
+                                         (1, 3, 1560, 16, 72)])
 def test_spatial_attention(impl, B, T, S, H, dh):
     out, want, a = spatial_case(B, T, S, H, dh, impl)
     check_close(out, want, ("spatial", impl, B, T, S, H, dh))
 
 
-@pytest.mark.parametrize("impl", IMPLS, ids=["tcgen05", "simt"])
+@pytest.mark.parametrize("impl", [kernels.IMPL_TCGEN05, kernels.IMPL_TC_SPLIT], ids=["tcgen05", "tc_split"])
+def test_attention_rising_scores_rescale(impl):
+    # key norms grow along the sequence, so later KV tiles raise the running max by far
+    # more than 2^8: exercises the lazy O rescale of the online softmax
+    g = torch.Generator(device=DEV).manual_seed(5)
+    B, S, H, dh = 1, 1000, 2, 72
+    D = H * dh
+    q = torch.randn(B * S, D, device=DEV, generator=g)
+    k = torch.randn(B * S, D, device=DEV, generator=g) * torch.linspace(0.2, 6.0, S, device=DEV)[:, None]
+    v = torch.randn(B * S, D, device=DEV, generator=g)
+    q, k, v = (x.to(torch.bfloat16) for x in (q, k, v))
+    out = torch.full((B * S, D), float("nan"), device=DEV, dtype=torch.bfloat16)
+    st = (S * D, 0, D)
+    a = kernels.attn_args(q, k, v, out, st, st, st, st, B, 1, S, S, H, dh)
+    kernels.attention(a, impl)
+    torch.cuda.synchronize()
+    hv = lambda x: x.view(B, S, H, dh).transpose(1, 2)  # noqa: E731
+    want = ref_attention(hv(q), hv(k), hv(v)).transpose(1, 2).reshape(B * S, D)
+    check_close(out, want, ("rising", impl))
+
+
+@pytest.mark.parametrize("impl", IMPLS, ids=IMPL_IDS)
 @pytest.mark.parametrize("B,T,S,H,dh", [(2, 16, 100, 2, 72), (1, 8, 64, 2, 72), (1, 32, 40, 2, 72),
                                          (2, 4, 16, 4, 8), (1, 24, 30, 2, 16), (1, 16, 1560, 1, 72)])
 def test_temporal_attention(impl, B, T, S, H, dh):
@@ -98,9 +121,9 @@ def test_temporal_attention(impl, B, T, S, H, dh):
     check_close(out, want, ("temporal", impl, B, T, S, H, dh))
 
 
-@pytest.mark.parametrize("impl", IMPLS, ids=["tcgen05", "simt"])
+@pytest.mark.parametrize("impl", IMPLS, ids=IMPL_IDS)
 @pytest.mark.parametrize("B,N,M,H,dh", [(2, 2048, 300, 2, 72), (2, 1000, 120, 2, 72), (1, 64, 16, 2, 72),
-                                         (2, 64, 8, 4, 8), (1, 500, 5, 2, 16)])
+                                         (2, 64, 8, 4, 8), (1, 500, 5, 2, 16), (2, 24960, 300, 16, 72)])
 def test_cross_attention(impl, B, N, M, H, dh):
     out, want, a = cross_case(B, N, M, H, dh, impl)
     check_close(out, want, ("cross", impl, B, N, M, H, dh))
