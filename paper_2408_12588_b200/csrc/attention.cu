@@ -17,6 +17,7 @@ int attn_tc_launch(const pab_attn_args* a, cudaStream_t st);  // attn_tc.cu
 bool attn_tc_supported(const pab_attn_args* a);                 // attn_tc.cu
 int attn_tc_packing(const pab_attn_args* a);                    // attn_tc.cu: >0 = packed short sequences
 int attn_fa_launch(const pab_attn_args* a, cudaStream_t st);  // attn_fa.cu
+bool attn_fa_supported(const pab_attn_args* a);                // attn_fa.cu
 
 namespace {
 
@@ -124,7 +125,7 @@ extern "C" int pab_attention(const pab_attn_args* a, int impl, void* stream) {
         // long sequences: row-per-thread kernel (attn_fa.cu); short packed sequences
         // (temporal attention): block-diagonal kernel (attn_tc.cu)
         if (!attn_tc_supported(a)) return PAB_ERR_UNSUPPORTED;
-        return attn_tc_packing(a) ? attn_tc_launch(a, st) : attn_fa_launch(a, st);
+        return (attn_tc_packing(a) || !attn_fa_supported(a)) ? attn_tc_launch(a, st) : attn_fa_launch(a, st);
     }
     if (impl == 3) {  // previous split-row kernel for every shape (A/B comparisons)
         if (!attn_tc_supported(a)) return PAB_ERR_UNSUPPORTED;

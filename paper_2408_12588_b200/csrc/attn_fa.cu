@@ -6,28 +6,30 @@
 // (pkg/src/pab_engine/model.py:346-359, 376-385):
 //   logits = q k^T * (1/sqrt(dh)); p = softmax(logits) (max-shifted); out = p v
 //
-// CTA (512 threads, one persistent CTA per SM, two 128-row query tiles per work item
-// sharing every K/V tile):
-//   warps 0-3   softmax of query tile 0, one thread per query row (= TMEM lane)
-//   warps 4-7   softmax of query tile 1
-//   warps 8-11  epilogue: O / l -> bf16 rows in global memory (both tiles)
-//   warp  12    MMA issuer (one elected lane; also owns the TMEM allocation)
-//   warp  13    TMA producer (one elected lane)
-//   warps 14-15 idle (register donors for setmaxnreg)
-// TMEM (512 columns): S_t at [128t, 128t + 128), P_t (bf16 pairs) over the first
-// 64 columns of S_t, O_t at [256 + 128t, 256 + 128t + dh_pad).
+// CTA (384 threads, one persistent CTA per SM; a work item is two 128-row query tiles
+// of one (problem, head) that share every K/V tile):
+//   warps 0-3   softmax + epilogue of query tile 0, one thread per query row (= TMEM lane)
+//   warps 4-7   softmax + epilogue of query tile 1
+//   warp  8     MMA issuer (lane 0 issues every tcgen05.mma; warp 8 owns TMEM)
+//   warp  9     TMA producer (lane 0)
+//   warp  10    V fixer: writes 1.0 into the first padded V column (see row sums)
+//   warp  11    idle
 //
-// Per tile t and KV tile j the MMA warp issues  O_t += P_t(j) V_j  (A operand = P
-// straight from TMEM) followed by  S_t(j+1) = Q_t K_{j+1}^T  which overwrites the
-// P_t(j) columns; tcgen05 MMAs of one thread execute in issue order, so the PV
-// read completes before the next S lands.  While softmax t works on S_t(j+1) the
-// tensor pipe runs the other tile's PV/S pair, so MMA and exp2 overlap.
+// TMEM (512 columns), KV tiles of 112 keys so that S, P and O of both tiles fit side by
+// side (no aliasing):  S_t [112t, 112t + 112),  O_t [224 + OC t, ...),  P_t [384 + 64t, +56).
+// Because P does not overwrite S, the MMA warp issues S(j+1) = Q K_{j+1}^T as soon as
+// the softmax has pulled S(j) into registers, i.e. while it is still exponentiating,
+// and PV(j) when P(j) is stored.  The two tiles run in phase, so the MMA warp issues
+// S_0/S_1 and PV_0/PV_1 with their K-steps interleaved: tcgen05 MMAs on one accumulator
+// serialise at ~80 cycles each, two independent accumulators keep the tensor pipe full.
 //
-// Online softmax: each thread holds its row's 128 scores in registers; the running
-// max is only raised (and O rescaled in place in TMEM) when a tile's max exceeds it
-// by more than 2^8, so P <= 256 in bf16 and the O correction is rare.  exp2 runs on
-// MUFU for most columns and on the FMA pipe (degree-3 polynomial on f32x2 pairs) for
-// one pair in PAB_FA_POLY_DIV, balancing the two pipes.
+// Row sums: the V fixer stores 1.0 into V column dh (zero padding otherwise), so the
+// PV MMA accumulates sum_k P[r, k] into O[r, dh] -- the softmax does no row-sum
+// arithmetic and the normaliser is the sum of exactly the bf16 P values multiplied
+// into O.  Online softmax: the running max is only raised (and O rescaled in TMEM)
+// when a tile's max exceeds it by more than 2^8, so P <= 256 and the rescale is rare.
+// exp2 runs on MUFU for most columns and on the FMA pipe (degree-3 polynomial on f32x2
+// pairs) for one pair in PAB_FA_POLY_DIV.
 #include "tc_ptx.cuh"
 
 namespace pab {
@@ -38,24 +40,18 @@ namespace fa {
 
 using namespace pab::tc;
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 384;
 constexpr int kRows = 128;   // query rows per tile == TMEM lanes
-constexpr int kKv = 128;     // keys per KV tile
-constexpr int kMmaWarp = 12;
-constexpr int kTmaWarp = 13;
-constexpr int kEpiWarp0 = 8;
+constexpr int kKv = 112;     // keys per KV tile
+constexpr int kMmaWarp = 8;
+constexpr int kTmaWarp = 9;
+constexpr int kFixWarp = 10;
 constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kSCol = 0, kPCol = 384;
 
 #ifndef PAB_FA_POLY_DIV
 #define PAB_FA_POLY_DIV 4   // one column pair in PAB_FA_POLY_DIV on the FMA pipe (0: MUFU only)
 #endif
-#ifndef PAB_FA_SOFTMAX_REGS
-#define PAB_FA_SOFTMAX_REGS 200
-#endif
-#ifndef PAB_FA_OTHER_REGS
-#define PAB_FA_OTHER_REGS 56
-#endif
-static_assert(2 * 128 * PAB_FA_SOFTMAX_REGS + 2 * 128 * PAB_FA_OTHER_REGS <= 65536, "register file");
 
 struct Params {
     int n_q, n_k, n_b, heads, dh;
@@ -75,46 +71,38 @@ struct Params {
     do {                           \
     } while (0)
 #else
-#define FA_TRACE(cond, itn, t, ev)                                                        \
-    do {                                                                                  \
-        if (p.trace != nullptr && (cond) && blockIdx.x == 0 && (itn) < 64)                \
-            p.trace[((itn) * 2 + (t)) * 16 + (ev)] = clock64();                           \
+#define FA_TRACE(cond, itn, t, ev)                                         \
+    do {                                                                   \
+        if (p.trace != nullptr && (cond) && blockIdx.x == 0 && (itn) < 64) \
+            p.trace[((itn) * 2 + (t)) * 16 + (ev)] = clock64();            \
     } while (0)
 #endif
 
-template <int N128, int N32>
+// N128 x 64 + N32 x 16 = dh rounded up to 16 (the QK^T reduction); NV = V atoms of 16
+// columns = dh / 16 + 1 (always one padded column for the row sum)
+template <int N128, int N32, int NV>
 struct Geometry {
-    static constexpr int kDhPad = 64 * N128 + 16 * N32;
-    static constexpr int kTileBytes = N128 * 16384 + N32 * 4096;  // one 128-row operand tile
-    static constexpr int kQ0 = 0;                                 // 2 item buffers x 2 tiles
-    static constexpr int kK0 = 4 * kTileBytes;                    // 3-stage K ring
-    static constexpr int kV0 = 7 * kTileBytes;                    // 3-stage V ring
-    static constexpr int kL0 = 10 * kTileBytes;                   // final row sums [tile][row]
-    static constexpr int kBar = kL0 + 2 * kRows * 4;
+    static constexpr int kDhK = 64 * N128 + 16 * N32;
+    static constexpr int kOCols = 16 * NV;
+    static constexpr int kSlot = 20480;  // one 128-row operand slot (Q, K or V), any dh <= 80
+    static constexpr int kQ0 = 0;        // 2 item buffers x 2 tiles
+    static constexpr int kK0 = 4 * kSlot;  // 3-stage K ring
+    static constexpr int kV0 = 7 * kSlot;  // 3-stage V ring
+    static constexpr int kBar = 10 * kSlot;
     static constexpr int kSmem = kBar + 512 + 1024;  // + barriers + alignment slack
+    static constexpr uint32_t kOCol0 = 224, kOStride = kOCols;
+    static_assert(N128 * 16384 + N32 * 4096 <= kSlot && NV * 4096 <= kSlot, "operand slot");
+    static_assert(kOCol0 + 2 * kOCols <= kPCol, "O tiles overlap P in TMEM");
     static_assert(kSmem <= 232448, "attention tiles exceed the 227 KB shared memory of one CTA");
-    static_assert(kDhPad <= 128, "O tiles exceed TMEM");
 };
 
 struct Bars {
-    uint64_t q_full[2], q_empty[2], k_full[3], k_empty[3], v_full[3], v_empty[3];
-    uint64_t s_full[2], p_full[2], o_full[2], o_free[2], l_full[2];
-    uint32_t tmem_base;
+    uint64_t q_full[2], q_empty[2], k_full[3], k_empty[3], v_full[3], v_ready[3], v_empty[3];
+    uint64_t s_full, s_free, p_full, o_done;
 };
 
-__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                          uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-
-// single-thread issue (the MMA loop runs on lane 0 of the MMA warp): descriptors are
-// passed as (lo, hi) words so advancing a K step is one 32-bit add on the lo word
+// single-thread tcgen05.mma issue (lane 0 of the MMA warp): descriptors are passed as
+// (lo, hi) words so advancing a K step is one 32-bit add on the lo word
 __device__ __forceinline__ void mma_ss1(uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo, uint32_t b_hi,
                                        uint32_t idesc, uint32_t accumulate) {
     asm volatile(
@@ -141,15 +129,87 @@ __device__ __forceinline__ void commit1(uint64_t* bar) {
                  : "memory");
 }
 
+// Whole MMA groups in one asm statement (one elect for the group, descriptor arithmetic
+// on the 64-bit descriptors inside the asm): the per-MMA issue cost of compiler-generated
+// code (R2UR moves + an ELECT loop per instruction, ~100 cycles each) otherwise exceeds
+// the tensor-pipe time of the MMA itself.  Geometry of dh = 72: 4 SW128 K-steps + 1 SW32.
+// S_t = Q_t K^T for both tiles, K-steps interleaved (tile 1 only when `two`).
+__device__ __forceinline__ void mma_group_s_72(uint32_t d0, uint32_t d1, uint64_t q128, uint64_t k128, uint64_t q32,
+                                              uint64_t k32, uint32_t idesc, uint32_t two, uint32_t qstride) {
+    asm volatile(
+        "{\n\t.reg .pred e, e2, pf, pt;\n\t.reg .b64 qa, ka, qs;\n\t"
+        "setp.ne.b32 pt, %8, 0;\n\t"   // pt = two (reassigned to true below)
+        "setp.ne.b32 pf, %7, %7;\n\t"  // false
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "and.pred e2, e, pt;\n\t"
+        "setp.eq.b32 pt, %7, %7;\n\t"  // true
+        "cvt.u64.u32 qs, %9;\n\t"
+        // k = 0 (SW128, +0)
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %6, pf;\n\t"
+        "add.s64 qa, %2, qs;\n\t"
+        "@e2 tcgen05.mma.cta_group::1.kind::f16 [%1], qa, %3, %6, pf;\n\t"
+        // k = 1..3 (SW128, +32 B per step -> +2 in the descriptor)
+        "add.s64 qa, %2, 2;\n\tadd.s64 ka, %3, 2;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], qa, ka, %6, pt;\n\t"
+        "add.s64 qa, qa, qs;\n\t"
+        "@e2 tcgen05.mma.cta_group::1.kind::f16 [%1], qa, ka, %6, pt;\n\t"
+        "add.s64 qa, %2, 4;\n\tadd.s64 ka, %3, 4;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], qa, ka, %6, pt;\n\t"
+        "add.s64 qa, qa, qs;\n\t"
+        "@e2 tcgen05.mma.cta_group::1.kind::f16 [%1], qa, ka, %6, pt;\n\t"
+        "add.s64 qa, %2, 6;\n\tadd.s64 ka, %3, 6;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], qa, ka, %6, pt;\n\t"
+        "add.s64 qa, qa, qs;\n\t"
+        "@e2 tcgen05.mma.cta_group::1.kind::f16 [%1], qa, ka, %6, pt;\n\t"
+        // k = 4 (SW32 block)
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %4, %5, %6, pt;\n\t"
+        "add.s64 qa, %4, qs;\n\t"
+        "@e2 tcgen05.mma.cta_group::1.kind::f16 [%1], qa, %5, %6, pt;\n\t}" ::"r"(d0),
+        "r"(d1), "l"(q128), "l"(k128), "l"(q32), "l"(k32), "r"(idesc), "r"(0), "r"(two), "r"(qstride)
+        : "memory");
+}
+// O_t += P_t V for both tiles: `steps` (<= 7) K-steps of 16 keys, A = P_t from TMEM
+// (+8 columns per step), B = V atoms (+512 B per step -> +32 in the descriptor)
+__device__ __forceinline__ void mma_group_pv7(uint32_t o0, uint32_t o1, uint32_t p0, uint32_t p1, uint64_t v,
+                                             uint32_t idesc, uint32_t accumulate, uint32_t two, uint32_t steps) {
+    asm volatile(
+        "{\n\t.reg .pred e, e2, pa, pt, s1, s2, s3, s4, s5, s6;\n\t.reg .b64 vb;\n\t.reg .b32 pa0, pa1;\n\t"
+        "setp.ne.b32 pt, %7, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "and.pred e2, e, pt;\n\t"
+        "setp.ne.b32 pa, %6, 0;\n\t"
+        "setp.eq.b32 pt, %7, %7;\n\t"
+        "setp.gt.u32 s1, %8, 1;\n\tsetp.gt.u32 s2, %8, 2;\n\tsetp.gt.u32 s3, %8, 3;\n\t"
+        "setp.gt.u32 s4, %8, 4;\n\tsetp.gt.u32 s5, %8, 5;\n\tsetp.gt.u32 s6, %8, 6;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %4, %5, pa;\n\t"
+        "@e2 tcgen05.mma.cta_group::1.kind::f16 [%1], [%3], %4, %5, pa;\n\t"
+#define PAB_PV_STEP(S, VOFF, POFF)                                                                        \
+        "add.s64 vb, %4, " #VOFF ";\n\tadd.u32 pa0, %2, " #POFF ";\n\tadd.u32 pa1, %3, " #POFF ";\n\t" \
+        "and.pred " #S ", " #S ", e;\n\t"                                                 \
+        "@" #S " tcgen05.mma.cta_group::1.kind::f16 [%0], [pa0], vb, %5, pt;\n\t"        \
+        "and.pred " #S ", " #S ", e2;\n\t"                                                \
+        "@" #S " tcgen05.mma.cta_group::1.kind::f16 [%1], [pa1], vb, %5, pt;\n\t"
+        PAB_PV_STEP(s1, 32, 8) PAB_PV_STEP(s2, 64, 16) PAB_PV_STEP(s3, 96, 24) PAB_PV_STEP(s4, 128, 32)
+        PAB_PV_STEP(s5, 160, 40) PAB_PV_STEP(s6, 192, 48)
+#undef PAB_PV_STEP
+        "}" ::"r"(o0), "r"(o1), "r"(p0), "r"(p1), "l"(v), "r"(idesc), "r"(accumulate), "r"(two), "r"(steps)
+        : "memory");
+}
+
 __device__ __forceinline__ float max3(float a, float b, float c) {
     float r;
     asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
     return r;
 }
 
+#define PAB_TMEM_ST8U(taddr, r)                                                                          \
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), \
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])  \
+                 : "memory")
+
 // 2^x for a pair of floats on the FMA pipe: x = i + f with i = round(x) via the
 // 1.5*2^23 magic constant, 2^f by a degree-3 minimax polynomial on [-0.5, 0.5]
-// (max rel err 7.5e-5, far below the bf16 rounding of P), exponent add by LEA.
+// (max rel err 7.5e-5, far below the bf16 rounding of P), exponent add as an integer.
 __device__ __forceinline__ void poly_exp2_x2(float& a, float& b) {
     a = fmaxf(a, -127.0f);
     b = fmaxf(b, -127.0f);
@@ -165,64 +225,44 @@ __device__ __forceinline__ void poly_exp2_x2(float& a, float& b) {
     b = __int_as_float(__float_as_int(pv.y) + (__float_as_int(tv.y) << 23));
 }
 
-// 128 fp32 scores of this thread's row (TMEM lane) -> registers
-__device__ __forceinline__ void load_row128(uint32_t taddr, float* s) {
-    PAB_TMEM_LD32(taddr, s);
-    PAB_TMEM_LD32(taddr + 32, (s + 32));
-    PAB_TMEM_LD32(taddr + 64, (s + 64));
-    PAB_TMEM_LD32(taddr + 96, (s + 96));
-    tmem_wait_ld();
-}
-
-// P = exp2(s * scale_log2 - m) -> bf16 pairs into TMEM (16 columns per 32 scores);
-// returns the row-sum contribution.  MASKED: columns >= nv give P = 0.
-template <bool MASKED>
-__device__ __forceinline__ float exp_store_row(float* s, float scale_log2, float neg_m, uint32_t p_tmem, int nv) {
-    const unsigned long long sc2 = f2_pack(scale_log2, scale_log2), nm2 = f2_pack(neg_m, neg_m);
-    unsigned long long acc2[4] = {0ull, 0ull, 0ull, 0ull};
+// P = exp2(s * scale_log2 - m) for columns [c0, c0 + 2 NPAIRS) -> NPAIRS packed bf16 pairs
+template <bool MASKED, int NPAIRS>
+__device__ __forceinline__ void exp_pack(const float* s, int c0, unsigned long long sc2, unsigned long long nm2,
+                                         int nv, uint32_t* pk) {
 #pragma unroll
-    for (int ch = 0; ch < 4; ++ch) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            const int c = 32 * ch + 2 * q;
-            float2 x = f2_unpack(f2_fma(f2_pack(s[c], s[c + 1]), sc2, nm2));
-            if (PAB_FA_POLY_DIV > 0 && (q % (PAB_FA_POLY_DIV > 0 ? PAB_FA_POLY_DIV : 1)) ==
-                                           (PAB_FA_POLY_DIV > 0 ? PAB_FA_POLY_DIV : 1) - 1) {
-                poly_exp2_x2(x.x, x.y);
-            } else {
+    for (int q = 0; q < NPAIRS; ++q) {
+        const int c = c0 + 2 * q;
+        float2 x = f2_unpack(f2_fma(f2_pack(s[c], s[c + 1]), sc2, nm2));
+        if (PAB_FA_POLY_DIV > 0 && !MASKED &&
+            (q % (PAB_FA_POLY_DIV > 0 ? PAB_FA_POLY_DIV : 1)) == (PAB_FA_POLY_DIV > 0 ? PAB_FA_POLY_DIV : 1) - 1) {
+            poly_exp2_x2(x.x, x.y);
+        } else {
 #ifdef PAB_FA_DIAG_NOEXP  // timing diagnostic only: exp2 replaced by a multiply
-                x.x *= 0.5f;
-                x.y *= 0.5f;
+            x.x *= 0.5f;
+            x.y *= 0.5f;
 #else
-                x.x = fast_exp2(x.x);
-                x.y = fast_exp2(x.y);
+            x.x = fast_exp2(x.x);
+            x.y = fast_exp2(x.y);
 #endif
-            }
-            if (MASKED) {
-                x.x = (c < nv) ? x.x : 0.f;
-                x.y = (c + 1 < nv) ? x.y : 0.f;
-            }
-            acc2[q & 3] = f2_add(acc2[q & 3], f2_pack(x.x, x.y));
-            pk[q] = pack_bf16(x.x, x.y);
         }
-        PAB_TMEM_ST16U(p_tmem + 16 * ch, pk);
+        if (MASKED) {
+            x.x = (c < nv) ? x.x : 0.f;
+            x.y = (c + 1 < nv) ? x.y : 0.f;
+        }
+        pk[q] = pack_bf16(x.x, x.y);
     }
-    const unsigned long long a01 = f2_add(acc2[0], acc2[1]), a23 = f2_add(acc2[2], acc2[3]);
-    const float2 a = f2_unpack(f2_add(a01, a23));
-    return a.x + a.y;
 }
 
-template <int N128, int N32>
+template <int N128, int N32, int NV>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fa_kernel(const __grid_constant__ CUtensorMap q128, const __grid_constant__ CUtensorMap q32,
                    const __grid_constant__ CUtensorMap k128, const __grid_constant__ CUtensorMap k32,
                    const __grid_constant__ CUtensorMap v32, const Params p) {
-    using G = Geometry<N128, N32>;
+    using G = Geometry<N128, N32, NV>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     Bars* bars = reinterpret_cast<Bars*>(smem + G::kBar);
-    float* l_buf = reinterpret_cast<float*>(smem + G::kL0);
+    __shared__ uint32_t tmem_base_slot;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // item -> (head, pair, a, b), head fastest: concurrently running CTAs read all heads of
@@ -245,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     const int my_items = (p.n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
     const int n_kv = p.n_kv;
-    const uint32_t tile_bytes = (uint32_t)kRows * (uint32_t)(N128 * 128 + N32 * 32);
+    const int n_iters = my_items * n_kv;  // global (item, kv tile) iterations of this CTA
 
     // ---------------------------------------------------------------- setup
     if (warp == kTmaWarp && lane == 0) {
@@ -259,23 +299,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < 2; ++s) {
             mbar_init(&bars->q_full[s], 1);
             mbar_init(&bars->q_empty[s], 1);
-            mbar_init(&bars->s_full[s], 1);
-            mbar_init(&bars->p_full[s], 4);
-            mbar_init(&bars->o_full[s], 1);
-            mbar_init(&bars->o_free[s], 4);
-            mbar_init(&bars->l_full[s], 4);
         }
         for (int s = 0; s < 3; ++s) {
             mbar_init(&bars->k_full[s], 1);
             mbar_init(&bars->k_empty[s], 1);
             mbar_init(&bars->v_full[s], 1);
+            mbar_init(&bars->v_ready[s], 1);
             mbar_init(&bars->v_empty[s], 1);
         }
+        mbar_init(&bars->s_full, 1);
+        mbar_init(&bars->s_free, 8);  // one arrival per softmax warp (both tiles)
+        mbar_init(&bars->p_full, 8);
+        mbar_init(&bars->o_done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(&bars->tmem_base)),
+                         smem_u32(&tmem_base_slot)),
                      "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
@@ -286,60 +326,108 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t tmem = 0;
 
     if (warp < 8) {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(PAB_FA_SOFTMAX_REGS));
-        // ================================================= softmax of tile t
+        // ========================================= softmax + epilogue of query tile t
         const int t = warp >> 2;
         const int wl = warp & 3;
         const int row = wl * 32 + lane;
         const uint32_t lane_off = (uint32_t)(wl * 32) << 16;
-        const uint32_t s_tmem = tmem + lane_off + 128 * t;
-        const uint32_t o_tmem = tmem + lane_off + 256 + 128 * t;
+        const uint32_t s_tmem = tmem + lane_off + kSCol + kKv * t;
+        const uint32_t o_tmem = tmem + lane_off + G::kOCol0 + G::kOStride * t;
+        const uint32_t p_tmem = tmem + lane_off + kPCol + 64 * t;
         const int tail = p.n_k - (n_kv - 1) * kKv;  // live keys of the last KV tile
-        int it_n = 0;
+        const bool trc = (wl == 0 && lane == 0);
+        // O of the previous item of this tile -> normalised bf16 rows (its last P.V done)
+        auto epilogue = [&](const Item& it) {
+            float o[16];
+            PAB_TMEM_LD16(o_tmem + 16 * (p.dh / 16), o);  // row sum sits in column dh
+            tmem_wait_ld();
+            float l = o[0];
+#pragma unroll
+            for (int e = 1; e < 16; ++e) l = (e == p.dh % 16) ? o[e] : l;
+            const float inv = (l > 0.f) ? 1.0f / l : 0.f;
+            const int i = (it.tile0 + t) * kRows + row;
+            const bool store = i < p.n_q;
+            __nv_bfloat16* dst = p.o + (int64_t)it.a_idx * p.o_sa + (int64_t)it.b_idx * p.o_sb + (int64_t)i * p.o_si +
+                                 (int64_t)it.h * p.dh;
+#pragma unroll
+            for (int cc = 0; cc < NV; ++cc) {
+                if (16 * cc >= p.dh) break;
+                PAB_TMEM_LD16(o_tmem + 16 * cc, o);
+                tmem_wait_ld();
+                if (store) {
+#pragma unroll
+                    for (int e = 0; e < 16; e += 8) {
+                        if (16 * cc + e < p.dh) {
+                            uint32_t w[4];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) w[q] = pack_bf16(o[e + 2 * q] * inv, o[e + 2 * q + 1] * inv);
+                            *reinterpret_cast<uint4*>(dst + 16 * cc + e) = make_uint4(w[0], w[1], w[2], w[3]);
+                        }
+                    }
+                }
+            }
+        };
+        Item prev;
+        bool have_prev = false;
+        int gi = 0;
         for (int c = 0; c < my_items; ++c) {
             const Item it = decode((int)blockIdx.x + c * (int)gridDim.x);
-            if (t == 1 && !it.two) continue;
-            float m_run = -INFINITY, l_run = 0.f;
-            for (int j = 0; j < n_kv; ++j, ++it_n) {
-                const bool trc = (wl == 0 && lane == 0);
-                FA_TRACE(trc, it_n, t, 0);
-                mbar_wait(&bars->s_full[t], it_n & 1);
+            const bool active = (t == 0) || it.two;
+            float m_run = -INFINITY;
+            for (int j = 0; j < n_kv; ++j, ++gi) {
+                FA_TRACE(trc, gi, t, 0);
+                mbar_wait(&bars->s_full, gi & 1);
                 tc_fence_after();
-                FA_TRACE(trc, it_n, t, 1);
-                float s[128];
-                load_row128(s_tmem, s);
-                FA_TRACE(trc, it_n, t, 2);
-#ifdef PAB_FA_DIAG_NOSOFTMAX  // timing diagnostic only: MMA/TMA pipeline without softmax math
-                if (s[0] == 12345.f) l_run += 1.f;
+                FA_TRACE(trc, gi, t, 1);
+                if (!active) {
+                    // second tile absent: arrive on the pair's barriers with the same waits as
+                    // an active tile (o_done(gi - 1) before p_full(gi)), so these arrivals can
+                    // never run a phase ahead of tile 0's and complete a phase on their own
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bars->s_free);
+                    if (gi > 0) mbar_wait(&bars->o_done, (gi - 1) & 1);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bars->p_full);
+                    continue;
+                }
+                float s[kKv];
+                PAB_TMEM_LD32(s_tmem, s);
+                PAB_TMEM_LD32(s_tmem + 32, (s + 32));
+                PAB_TMEM_LD32(s_tmem + 64, (s + 64));
+                PAB_TMEM_LD16(s_tmem + 96, (s + 96));
+                tmem_wait_ld();
+                // S is in registers: the MMA warp may overwrite it with S(j+1)
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->p_full[t]);
-                continue;
-#endif
+                if (lane == 0) mbar_arrive(&bars->s_free);
+                FA_TRACE(trc, gi, t, 2);
                 const bool masked = (j == n_kv - 1) && (tail < kKv);
                 if (masked) {
 #pragma unroll
-                    for (int cc = 0; cc < 128; ++cc) s[cc] = (cc < tail) ? s[cc] : -INFINITY;
+                    for (int cc = 0; cc < kKv; ++cc) s[cc] = (cc < tail) ? s[cc] : -INFINITY;
                 }
                 // row max of the raw scores (scale > 0 commutes with max)
                 float m4[4];
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
-                    float m = fmaxf(s[32 * g], s[32 * g + 1]);
+                    float m = fmaxf(s[28 * g], s[28 * g + 1]);
 #pragma unroll
-                    for (int cc = 2; cc < 32; cc += 2) m = max3(m, s[32 * g + cc], s[32 * g + cc + 1]);
+                    for (int cc = 2; cc < 28; cc += 2) m = max3(m, s[28 * g + cc], s[28 * g + cc + 1]);
                     m4[g] = m;
                 }
                 const float m_tile = max3(fmaxf(m4[0], m4[1]), m4[2], m4[3]) * p.scale_log2;
                 const bool need = m_tile > m_run + 8.0f;
+                // PV(gi - 1) must be complete before O is rescaled or P is overwritten
+                bool waited = false;
                 if (__any_sync(0xffffffffu, need)) {
                     const float m_new = need ? m_tile : m_run;
                     if (j > 0) {
-                        // O holds sum_{j' < j}: complete, since S(j) was issued after PV(j-1)
+                        mbar_wait(&bars->o_done, (gi - 1) & 1);
+                        tc_fence_after();
+                        waited = true;
                         const float alpha = fast_exp2(m_run - m_new);
-                        l_run *= alpha;
 #pragma unroll 1
-                        for (int cc = 0; cc < G::kDhPad / 16; ++cc) {
+                        for (int cc = 0; cc < NV; ++cc) {
                             float o[16];
                             PAB_TMEM_LD16(o_tmem + 16 * cc, o);
                             tmem_wait_ld();
@@ -350,202 +438,229 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     m_run = m_new;
                 }
-                FA_TRACE(trc, it_n, t, 3);
+                FA_TRACE(trc, gi, t, 3);
                 const float neg_m = -m_run;
-                l_run += masked ? exp_store_row<true>(s, p.scale_log2, neg_m, s_tmem, tail)
-                                : exp_store_row<false>(s, p.scale_log2, neg_m, s_tmem, kKv);
-                FA_TRACE(trc, it_n, t, 4);
+                const unsigned long long sc2 = f2_pack(p.scale_log2, p.scale_log2), nm2 = f2_pack(neg_m, neg_m);
+                uint32_t pk[kKv / 2];
+                if (masked) {
+                    exp_pack<true, 16>(s, 0, sc2, nm2, tail, pk);
+                    exp_pack<true, 16>(s, 32, sc2, nm2, tail, pk + 16);
+                    exp_pack<true, 16>(s, 64, sc2, nm2, tail, pk + 32);
+                    exp_pack<true, 8>(s, 96, sc2, nm2, tail, pk + 48);
+                } else {
+                    exp_pack<false, 16>(s, 0, sc2, nm2, kKv, pk);
+                    exp_pack<false, 16>(s, 32, sc2, nm2, kKv, pk + 16);
+                    exp_pack<false, 16>(s, 64, sc2, nm2, kKv, pk + 32);
+                    exp_pack<false, 8>(s, 96, sc2, nm2, kKv, pk + 48);
+                }
+                FA_TRACE(trc, gi, t, 4);
+                if (!waited && gi > 0) {
+                    mbar_wait(&bars->o_done, (gi - 1) & 1);
+                    tc_fence_after();
+                }
+                if (j == 0 && have_prev) epilogue(prev);  // O of the previous item is final
+                PAB_TMEM_ST16U(p_tmem, pk);
+                PAB_TMEM_ST16U(p_tmem + 16, (pk + 16));
+                PAB_TMEM_ST16U(p_tmem + 32, (pk + 32));
+                PAB_TMEM_ST8U(p_tmem + 48, (pk + 48));
                 tmem_wait_st();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->p_full[t]);
-                FA_TRACE(trc, it_n, t, 5);
+                if (lane == 0) mbar_arrive(&bars->p_full);
+                FA_TRACE(trc, gi, t, 5);
             }
-            // row sums for the epilogue warps (same TMEM lane quarter)
-            l_buf[t * kRows + row] = l_run;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bars->l_full[t]);
-        }
-    } else if (warp < 12) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PAB_FA_OTHER_REGS));
-        // ================================================= epilogue (both tiles)
-        const int wl = warp & 3;
-        const int row = wl * 32 + lane;
-        const uint32_t lane_off = (uint32_t)(wl * 32) << 16;
-        int ic[2] = {0, 0};
-        for (int c = 0; c < my_items; ++c) {
-            const Item it = decode((int)blockIdx.x + c * (int)gridDim.x);
-            for (int t = 0; t < 2; ++t) {
-                if (t == 1 && !it.two) break;
-                const int par = ic[t] & 1;
-                mbar_wait(&bars->l_full[t], par);
-                mbar_wait(&bars->o_full[t], par);
-                tc_fence_after();
-                ++ic[t];
-                const float l = l_buf[t * kRows + row];
-                const float inv = (l > 0.f) ? 1.0f / l : 0.f;
-                const int i = (it.tile0 + t) * kRows + row;
-                const bool store = i < p.n_q;
-                __nv_bfloat16* dst = p.o + (int64_t)it.a_idx * p.o_sa + (int64_t)it.b_idx * p.o_sb +
-                                     (int64_t)i * p.o_si + (int64_t)it.h * p.dh;
-                const uint32_t o_tmem = tmem + lane_off + 256 + 128 * t;
-#pragma unroll
-                for (int cc = 0; cc < G::kDhPad / 16; ++cc) {
-                    float o[16];
-                    PAB_TMEM_LD16(o_tmem + 16 * cc, o);
-                    tmem_wait_ld();
-                    if (store) {
-#pragma unroll
-                        for (int e = 0; e < 16; e += 8) {
-                            if (16 * cc + e < p.dh) {
-                                uint32_t w[4];
-#pragma unroll
-                                for (int q = 0; q < 4; ++q) w[q] = pack_bf16(o[e + 2 * q] * inv, o[e + 2 * q + 1] * inv);
-                                *reinterpret_cast<uint4*>(dst + 16 * cc + e) = make_uint4(w[0], w[1], w[2], w[3]);
-                            }
-                        }
-                    }
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->o_free[t]);
+            if (active) {
+                prev = it;
+                have_prev = true;
             }
         }
-    } else {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PAB_FA_OTHER_REGS));
-        if (warp == kTmaWarp) {
-            // ===================================================== TMA producer
-            if (lane == 0) {
-                int g = 0;  // K/V tiles loaded so far
-                for (int c = 0; c < my_items; ++c) {
-                    const Item it = decode((int)blockIdx.x + c * (int)gridDim.x);
-                    const int qb = c & 1;
-                    if (c >= 2) mbar_wait(&bars->q_empty[qb], ((c >> 1) - 1) & 1);
-                    mbar_expect_tx(&bars->q_full[qb], (it.two ? 2u : 1u) * tile_bytes);
-                    for (int t = 0; t < (it.two ? 2 : 1); ++t) {
-                        uint8_t* dst = smem + G::kQ0 + (2 * qb + t) * G::kTileBytes;
-                        const int i0 = (it.tile0 + t) * kRows;
-                        for (int blk = 0; blk < N128; ++blk)
-                            tma_load_5d(dst + blk * 16384, &q128, &bars->q_full[qb], 64 * blk, it.h, i0, it.b_idx,
-                                        it.a_idx);
-                        for (int blk = 0; blk < N32; ++blk)
-                            tma_load_5d(dst + N128 * 16384 + blk * 4096, &q32, &bars->q_full[qb],
-                                        64 * N128 + 16 * blk, it.h, i0, it.b_idx, it.a_idx);
-                    }
-                    for (int j = 0; j < n_kv; ++j, ++g) {
-                        const int st = g % 3;
-                        if (g >= 3) mbar_wait(&bars->k_empty[st], ((g / 3) - 1) & 1);
-                        uint8_t* kd = smem + G::kK0 + st * G::kTileBytes;
-                        mbar_expect_tx(&bars->k_full[st], tile_bytes);
-                        for (int blk = 0; blk < N128; ++blk)
-                            tma_load_5d(kd + blk * 16384, &k128, &bars->k_full[st], 64 * blk, it.h, j * kKv, it.b_idx,
-                                        it.a_idx);
-                        for (int blk = 0; blk < N32; ++blk)
-                            tma_load_5d(kd + N128 * 16384 + blk * 4096, &k32, &bars->k_full[st], 64 * N128 + 16 * blk,
-                                        it.h, j * kKv, it.b_idx, it.a_idx);
-                        // V as 16-column SW32 atoms ([atom][row][32 B]): one MN-major descriptor
-                        // spans the whole padded head dim (N = kDhPad)
-                        if (g >= 3) mbar_wait(&bars->v_empty[st], ((g / 3) - 1) & 1);
-                        uint8_t* vd = smem + G::kV0 + st * G::kTileBytes;
-                        mbar_expect_tx(&bars->v_full[st], tile_bytes);
-                        for (int blk = 0; blk < G::kDhPad / 16; ++blk)
-                            tma_load_5d(vd + blk * 4096, &v32, &bars->v_full[st], 16 * blk, it.h, j * kKv, it.b_idx,
-                                        it.a_idx);
-                    }
-                }
-            }
-        } else if (warp == kMmaWarp && lane == 0) {
-            // ======================================== MMA issuer: one thread issues every tcgen05.mma
-            constexpr uint32_t idS128 = idesc_bf16(128, 128, 0);
-            constexpr uint32_t idO = idesc_bf16(128, G::kDhPad, 1);
-            // descriptor words: lo = (addr >> 4) | (LBO >> 4) << 16, hi = (SBO >> 4) | version | layout
-            const uint32_t q_lo = smem_u32(smem + G::kQ0) >> 4, k_lo = smem_u32(smem + G::kK0) >> 4;
-            const uint32_t v_lo = smem_u32(smem + G::kV0) >> 4;
-            // (smem_desc bit layout: SBO >> 4 at [32, 46), version 1 at bit 46, layout at [61, 64))
-            constexpr uint32_t kHi128 = (1024u >> 4) | (1u << 14) | (kLayoutSW128 << 29);
-            constexpr uint32_t kHi32 = (256u >> 4) | (1u << 14) | (kLayoutSW32 << 29);
-            constexpr uint32_t kLbo16 = (16u >> 4) << 16;
-            // V: MN-major SW32, 16-column atoms 4096 B apart (LBO), 8-row groups 256 B apart (SBO)
-            constexpr uint32_t kLboV = (4096u >> 4) << 16;
-            auto cols_of = [&](int j) {
-                const int n = min(kKv, p.n_k - j * kKv);
-                return (n + 15) & ~15;
-            };
-            // S_t = Q_t K^T (K-major operands; ncols = key columns rounded up to 16)
-            auto issue_s = [&](int t, int qslot, int kst, int ncols) {
-                const uint32_t qa = q_lo + ((qslot * G::kTileBytes) >> 4), ka = k_lo + ((kst * G::kTileBytes) >> 4);
-                const uint32_t idS = (idS128 & ~(0x3Fu << 17)) | ((uint32_t)(ncols >> 3) << 17);
-                const uint32_t d_s = tmem + 128 * t;
-#pragma unroll
-                for (int blk = 0; blk < N128; ++blk)
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const uint32_t o = (blk * 16384 + 32 * k) >> 4;
-                        mma_ss1(d_s, (qa + o) | kLbo16, kHi128, (ka + o) | kLbo16, kHi128, idS, (blk | k) != 0);
-                    }
-#pragma unroll
-                for (int blk = 0; blk < N32; ++blk) {
-                    const uint32_t o = (N128 * 16384 + blk * 4096) >> 4;
-                    mma_ss1(d_s, (qa + o) | kLbo16, kHi32, (ka + o) | kLbo16, kHi32, idS, (N128 | blk) != 0);
-                }
-            };
-            // O_t += P_t V: ncols / 16 K-steps of 16 keys; A = P_t from TMEM (8 columns per step)
-            auto issue_pv = [&](int t, int vst, uint32_t accumulate, int ncols) {
-                const uint32_t va = v_lo + ((vst * G::kTileBytes) >> 4);
-                const uint32_t d_o = tmem + 256 + 128 * t, a_p = tmem + 128 * t;
-                if (ncols == kKv) {
-#pragma unroll
-                    for (int k = 0; k < kKv / 16; ++k)
-                        mma_ts1(d_o, a_p + 8 * k, (va + ((512 * k) >> 4)) | kLboV, kHi32, idO, accumulate | (k > 0));
-                } else {
-                    for (int k = 0; 16 * k < ncols; ++k)
-                        mma_ts1(d_o, a_p + 8 * k, (va + ((512 * k) >> 4)) | kLboV, kHi32, idO, accumulate | (k > 0));
-                }
-            };
-            int g = 0;                // K/V tiles consumed
-            int it_n[2] = {0, 0};     // softmax iterations per tile
-            int ic[2] = {0, 0};       // items per tile
+        if (have_prev) {
+            mbar_wait(&bars->o_done, (n_iters - 1) & 1);
+            tc_fence_after();
+            epilogue(prev);
+        }
+    } else if (warp == kTmaWarp) {
+        // ===================================================== TMA producer
+        if (lane == 0) {
+            constexpr uint32_t kQBytes = kRows * (N128 * 128 + N32 * 32);
+            constexpr uint32_t kKBytes = kKv * (N128 * 128 + N32 * 32);
+            constexpr uint32_t kVBytes = kKv * NV * 32;
+            int g = 0;  // K/V tiles loaded so far
             for (int c = 0; c < my_items; ++c) {
                 const Item it = decode((int)blockIdx.x + c * (int)gridDim.x);
                 const int qb = c & 1;
-                const int nt = it.two ? 2 : 1;
-                mbar_wait(&bars->q_full[qb], (c >> 1) & 1);
-                mbar_wait(&bars->k_full[g % 3], (g / 3) & 1);
-                tc_fence_after();
-                for (int t = 0; t < nt; ++t) {
-                    issue_s(t, 2 * qb + t, g % 3, cols_of(0));
-                    commit1(&bars->s_full[t]);
+                if (c >= 2) mbar_wait(&bars->q_empty[qb], ((c >> 1) - 1) & 1);
+                mbar_expect_tx(&bars->q_full[qb], (it.two ? 2u : 1u) * kQBytes);
+                for (int t = 0; t < (it.two ? 2 : 1); ++t) {
+                    uint8_t* dst = smem + G::kQ0 + (2 * qb + t) * G::kSlot;
+                    const int i0 = (it.tile0 + t) * kRows;
+                    for (int blk = 0; blk < N128; ++blk)
+                        tma_load_5d(dst + blk * 16384, &q128, &bars->q_full[qb], 64 * blk, it.h, i0, it.b_idx,
+                                    it.a_idx);
+                    for (int blk = 0; blk < N32; ++blk)
+                        tma_load_5d(dst + N128 * 16384 + blk * 4096, &q32, &bars->q_full[qb], 64 * N128 + 16 * blk,
+                                    it.h, i0, it.b_idx, it.a_idx);
                 }
-                commit1(&bars->k_empty[g % 3]);
-                if (n_kv == 1) commit1(&bars->q_empty[qb]);
-                for (int j = 0; j < n_kv; ++j) {
-                    const int gv = g + j;
-                    mbar_wait(&bars->v_full[gv % 3], (gv / 3) & 1);
-                    if (j + 1 < n_kv) mbar_wait(&bars->k_full[(gv + 1) % 3], ((gv + 1) / 3) & 1);
+                for (int j = 0; j < n_kv; ++j, ++g) {
+                    const int st = g % 3;
+                    if (g >= 3) mbar_wait(&bars->k_empty[st], ((g / 3) - 1) & 1);
+                    uint8_t* kd = smem + G::kK0 + st * G::kSlot;
+                    mbar_expect_tx(&bars->k_full[st], kKBytes);
+                    for (int blk = 0; blk < N128; ++blk)
+                        tma_load_5d(kd + blk * 16384, &k128, &bars->k_full[st], 64 * blk, it.h, j * kKv, it.b_idx,
+                                    it.a_idx);
+                    for (int blk = 0; blk < N32; ++blk)
+                        tma_load_5d(kd + N128 * 16384 + blk * 4096, &k32, &bars->k_full[st], 64 * N128 + 16 * blk,
+                                    it.h, j * kKv, it.b_idx, it.a_idx);
+                    // V as 16-column SW32 atoms ([atom][row][32 B], atoms 4 KB apart): one MN-major
+                    // descriptor spans the padded head dim; atom NV-1 holds the row-sum column
+                    if (g >= 3) mbar_wait(&bars->v_empty[st], ((g / 3) - 1) & 1);
+                    uint8_t* vd = smem + G::kV0 + st * G::kSlot;
+                    mbar_expect_tx(&bars->v_full[st], kVBytes);
+                    for (int blk = 0; blk < NV; ++blk)
+                        tma_load_5d(vd + blk * 4096, &v32, &bars->v_full[st], 16 * blk, it.h, j * kKv, it.b_idx,
+                                    it.a_idx);
+                }
+            }
+        }
+    } else if (warp == kFixWarp) {
+        // ====================================== V fixer: V[:, dh] = 1 (zero-filled by TMA)
+        // SW32 atom layout: row r at 32 r, 16-byte chunk index XOR (r >> 2) & 1
+        const int col = p.dh % 16;
+        const uint32_t atom_off = (uint32_t)(p.dh / 16) * 4096u;
+        for (int g = 0; g < n_iters; ++g) {
+            const int st = g % 3;
+            mbar_wait(&bars->v_full[st], (g / 3) & 1);
+            uint8_t* vd = smem + G::kV0 + st * G::kSlot + atom_off;
+#pragma unroll
+            for (int r = lane; r < kKv; r += 32) {
+                const uint32_t chunk = (uint32_t)(col >> 3) ^ (uint32_t)((r >> 2) & 1);
+                *reinterpret_cast<__nv_bfloat16*>(vd + r * 32 + chunk * 16 + (col & 7) * 2) =
+                    __float2bfloat16_rn(1.0f);
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->v_ready[st]);
+        }
+    } else if (warp == kMmaWarp) {
+        // ============================ MMA issuer (warp-converged; one elected lane issues the MMAs)
+        constexpr uint32_t idS128 = idesc_bf16(128, kKv, 0);
+        constexpr uint32_t idO = idesc_bf16(128, G::kOCols, 1);
+        // descriptor words: lo = (addr >> 4) | (LBO >> 4) << 16, hi = (SBO >> 4) | version | layout
+        // (smem_desc bit layout: SBO >> 4 at [32, 46), version 1 at bit 46, layout at [61, 64))
+        const uint32_t q_lo = smem_u32(smem + G::kQ0) >> 4, k_lo = smem_u32(smem + G::kK0) >> 4;
+        const uint32_t v_lo = smem_u32(smem + G::kV0) >> 4;
+        constexpr uint32_t kHi128 = (1024u >> 4) | (1u << 14) | (kLayoutSW128 << 29);
+        constexpr uint32_t kHi32 = (256u >> 4) | (1u << 14) | (kLayoutSW32 << 29);
+        constexpr uint32_t kLbo16 = (16u >> 4) << 16;
+        // V: MN-major SW32, 16-column atoms 4096 B apart (LBO), 8-row groups 256 B apart (SBO)
+        constexpr uint32_t kLboV = (4096u >> 4) << 16;
+        auto cols_of = [&](int j) {
+            const int n = min(kKv, p.n_k - j * kKv);
+            return (n + 15) & ~15;
+        };
+        // S_t = Q_t K^T for the active tiles, K-steps interleaved across the two accumulators
+        auto issue_s = [&](int qb, int kst, int ncols, int nt) {
+            const uint32_t ka = k_lo + ((kst * G::kSlot) >> 4);
+            const uint32_t idS = (idS128 & ~(0x3Fu << 17)) | ((uint32_t)(ncols >> 3) << 17);
+            if (N128 == 1 && N32 == 1) {
+                const uint32_t qa = q_lo + ((2 * qb * G::kSlot) >> 4);
+                const uint64_t dq = ((uint64_t)kHi128 << 32) | (qa | kLbo16), dk = ((uint64_t)kHi128 << 32) | (ka | kLbo16);
+                const uint64_t dq32 = ((uint64_t)kHi32 << 32) | ((qa + (16384 >> 4)) | kLbo16);
+                const uint64_t dk32 = ((uint64_t)kHi32 << 32) | ((ka + (16384 >> 4)) | kLbo16);
+                mma_group_s_72(tmem + kSCol, tmem + kSCol + kKv, dq, dk, dq32, dk32, idS, nt == 2, G::kSlot >> 4);
+                return;
+            }
+            if (lane != 0) return;
+#pragma unroll
+            for (int blk = 0; blk < N128; ++blk)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t o = (blk * 16384 + 32 * k) >> 4;
                     for (int t = 0; t < nt; ++t) {
-                        FA_TRACE(true, it_n[t], t, 10);
-                        mbar_wait(&bars->p_full[t], it_n[t] & 1);
-                        FA_TRACE(true, it_n[t], t, 8);
-                        if (j == 0 && ic[t] > 0) mbar_wait(&bars->o_free[t], (ic[t] - 1) & 1);
-                        tc_fence_after();
-                        issue_pv(t, gv % 3, j > 0, cols_of(j));
-                        if (j + 1 < n_kv) {
-                            issue_s(t, 2 * qb + t, (gv + 1) % 3, cols_of(j + 1));
-                            commit1(&bars->s_full[t]);
-                        } else {
-                            commit1(&bars->o_full[t]);
-                        }
-                        FA_TRACE(true, it_n[t], t, 9);
-                        ++it_n[t];
-                    }
-                    commit1(&bars->v_empty[gv % 3]);
-                    if (j + 1 < n_kv) {
-                        commit1(&bars->k_empty[(gv + 1) % 3]);
-                        if (j + 2 == n_kv) commit1(&bars->q_empty[qb]);
+                        const uint32_t qa = q_lo + (((2 * qb + t) * G::kSlot) >> 4);
+                        mma_ss1(tmem + kSCol + kKv * t, (qa + o) | kLbo16, kHi128, (ka + o) | kLbo16, kHi128, idS,
+                                (blk | k) != 0);
                     }
                 }
-                for (int t = 0; t < nt; ++t) ++ic[t];
-                g += n_kv;
+#pragma unroll
+            for (int blk = 0; blk < N32; ++blk) {
+                const uint32_t o = (N128 * 16384 + blk * 4096) >> 4;
+                for (int t = 0; t < nt; ++t) {
+                    const uint32_t qa = q_lo + (((2 * qb + t) * G::kSlot) >> 4);
+                    mma_ss1(tmem + kSCol + kKv * t, (qa + o) | kLbo16, kHi32, (ka + o) | kLbo16, kHi32, idS,
+                            (N128 | blk) != 0);
+                }
+            }
+        };
+        // O_t += P_t V: ncols / 16 K-steps of 16 keys; A = P_t from TMEM (8 columns per step)
+        auto issue_pv = [&](int vst, uint32_t accumulate, int ncols, int nt) {
+            const uint32_t va = v_lo + ((vst * G::kSlot) >> 4);
+            if (kKv / 16 == 7) {
+                const uint64_t dv = ((uint64_t)kHi32 << 32) | (va | kLboV);
+                mma_group_pv7(tmem + G::kOCol0, tmem + G::kOCol0 + G::kOStride, tmem + kPCol, tmem + kPCol + 64, dv, idO,
+                              accumulate, nt == 2, ncols / 16);
+                return;
+            }
+            if (lane != 0) return;
+            for (int k = 0; 16 * k < ncols; ++k)
+                for (int t = 0; t < nt; ++t)
+                    mma_ts1(tmem + G::kOCol0 + G::kOStride * t, tmem + kPCol + 64 * t + 8 * k,
+                            (va + ((512 * k) >> 4)) | kLboV, kHi32, idO, accumulate | (k > 0));
+        };
+        // iteration gi = (item c, kv tile j); S(gi + 1) is issued as soon as the softmax has
+        // read S(gi), PV(gi) when P(gi) is stored
+        int c = 0, j = 0, g = 0;
+        Item it = decode((int)blockIdx.x);
+        int nt = it.two ? 2 : 1;
+        if (my_items > 0) {
+            mbar_wait(&bars->q_full[0], 0);
+            mbar_wait(&bars->k_full[0], 0);
+            tc_fence_after();
+            issue_s(0, 0, cols_of(0), nt);
+            tc_commit(&bars->s_full);
+            tc_commit(&bars->k_empty[0]);
+            if (n_kv == 1) tc_commit(&bars->q_empty[0]);
+        }
+        for (int gi = 0; gi < n_iters; ++gi) {
+            // ---- S of the next iteration (may belong to the next item)
+            if (gi + 1 < n_iters) {
+                int c1 = c, j1 = j + 1;
+                if (j1 == n_kv) {
+                    c1 = c + 1;
+                    j1 = 0;
+                }
+                const Item it1 = (c1 == c) ? it : decode((int)blockIdx.x + c1 * (int)gridDim.x);
+                const int g1 = g + 1;
+                FA_TRACE(lane == 0, gi, 0, 10);
+                mbar_wait(&bars->s_free, gi & 1);
+                if (j1 == 0) mbar_wait(&bars->q_full[c1 & 1], (c1 >> 1) & 1);
+                mbar_wait(&bars->k_full[g1 % 3], (g1 / 3) & 1);
+                tc_fence_after();
+                FA_TRACE(lane == 0, gi, 0, 8);
+                issue_s(c1 & 1, g1 % 3, cols_of(j1), it1.two ? 2 : 1);
+                tc_commit(&bars->s_full);
+                tc_commit(&bars->k_empty[g1 % 3]);
+                if (j1 == n_kv - 1) tc_commit(&bars->q_empty[c1 & 1]);  // last S of item c1 issued
+            }
+            // ---- PV of this iteration
+            FA_TRACE(lane == 0, gi, 1, 10);
+            mbar_wait(&bars->p_full, gi & 1);
+            mbar_wait(&bars->v_ready[g % 3], (g / 3) & 1);
+            tc_fence_after();
+            FA_TRACE(lane == 0, gi, 1, 8);
+            issue_pv(g % 3, j > 0, cols_of(j), nt);
+            tc_commit(&bars->o_done);
+            tc_commit(&bars->v_empty[g % 3]);
+            FA_TRACE(lane == 0, gi, 1, 9);
+            ++g;
+            if (++j == n_kv) {
+                j = 0;
+                ++c;
+                if (c < my_items) {
+                    it = decode((int)blockIdx.x + c * (int)gridDim.x);
+                    nt = it.two ? 2 : 1;
+                }
             }
         }
     }
@@ -556,13 +671,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-template <int N128, int N32>
+template <int N128, int N32, int NV>
 int launch(const pab_attn_args* a, cudaStream_t st) {
-    using G = Geometry<N128, N32>;
+    using G = Geometry<N128, N32, NV>;
     static bool attr_set = false;
     if (!attr_set) {
-        if (cudaFuncSetAttribute(attn_fa_kernel<N128, N32>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem) !=
-            cudaSuccess)
+        if (cudaFuncSetAttribute(attn_fa_kernel<N128, N32, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 G::kSmem) != cudaSuccess)
             return launch_status("attn_fa smem attribute");
         attr_set = true;
     }
@@ -606,24 +721,30 @@ int launch(const pab_attn_args* a, cudaStream_t st) {
         if (num_sms <= 0) num_sms = 148;
     }
     dim3 grid((unsigned)(p.n_items < num_sms ? p.n_items : num_sms));
-    attn_fa_kernel<N128, N32><<<grid, kThreads, G::kSmem, st>>>(mq128, mq32, mk128, mk32, mv32, p);
+    attn_fa_kernel<N128, N32, NV><<<grid, kThreads, G::kSmem, st>>>(mq128, mq32, mk128, mk32, mv32, p);
     return launch_status("attn_fa");
 }
 
 }  // namespace fa
 
-// non-packed attention (spatial, cross) with dh <= 80 and a multiple of 8
+bool attn_fa_supported(const pab_attn_args* a) { return a->dh % 8 == 0 && a->dh <= 72; }
+
+// non-packed attention (spatial, cross) with dh <= 72 and a multiple of 8
 int attn_fa_launch(const pab_attn_args* a, cudaStream_t st) {
     const int n128 = a->dh / 64;
     const int n32 = (a->dh - 64 * n128 + 15) / 16;
-#define PAB_FA(A, B) \
-    if (n128 == A && n32 == B) return fa::launch<A, B>(a, st)
-    PAB_FA(0, 1);
-    PAB_FA(0, 2);
-    PAB_FA(0, 3);
-    PAB_FA(0, 4);
-    PAB_FA(1, 0);
-    PAB_FA(1, 1);
+    const int nv = a->dh / 16 + 1;
+#define PAB_FA(A, B, C) \
+    if (n128 == A && n32 == B && nv == C) return fa::launch<A, B, C>(a, st)
+    PAB_FA(0, 1, 1);  // dh 8
+    PAB_FA(0, 1, 2);  // dh 16
+    PAB_FA(0, 2, 2);  // dh 24
+    PAB_FA(0, 2, 3);  // dh 32
+    PAB_FA(0, 3, 3);  // dh 40
+    PAB_FA(0, 3, 4);  // dh 48
+    PAB_FA(0, 4, 4);  // dh 56
+    PAB_FA(1, 0, 5);  // dh 64
+    PAB_FA(1, 1, 5);  // dh 72
 #undef PAB_FA
     return PAB_ERR_UNSUPPORTED;
 }

@@ -26,14 +26,20 @@ torch.cuda.synchronize()
 lib.pab_attn_debug_trace(None)
 tr = buf.view(64, 2, 16).cpu()
 t0 = int(tr[tr > 0].min())
-names = {0: "sm:wait_S", 1: "sm:S_ready", 2: "sm:S_loaded", 3: "sm:max_done", 4: "sm:P_stored", 5: "sm:p_full",
-         10: "mma:wait_P", 8: "mma:P_ok", 9: "mma:PV+S_issued"}
+names = {0: "sm:wait_S", 1: "sm:S_ready", 2: "sm:S_loaded", 3: "sm:max_done", 4: "sm:exp_done", 5: "sm:p_full"}
+# MMA events are logged under tile 0 (S issue) / tile 1 (PV issue)
+mma_names = {(0, 10): "mma:wait_sfree", (0, 8): "mma:S_go", (1, 10): "mma:wait_P", (1, 8): "mma:PV_go",
+             (1, 9): "mma:PV_issued"}
 ev = []
 for j in range(int(os.environ.get("TL_ITERS", "30"))):
     for t in range(2):
         for e, nm in names.items():
             v = int(tr[j, t, e])
             if v:
+                ev.append((v - t0, j, t, nm))
+        for (tt, e), nm in mma_names.items():
+            v = int(tr[j, tt, e])
+            if tt == t and v:
                 ev.append((v - t0, j, t, nm))
 prev = 0
 for v, j, t, nm in sorted(ev):

@@ -31,10 +31,18 @@ __global__ void __launch_bounds__(256, 1) probe(int mode, int iters, long long* 
     __shared__ volatile int done;
     if (threadIdx.x == 0) done = 0;
     __syncthreads();
-    if (warp >= 4 && (mode == 7 || mode == 8)) {
+    if (warp >= 4 && (mode == 7 || mode == 8 || mode == 21)) {
         // TMEM traffic of the softmax warps: ld 128 S columns (+ st 64 P columns in mode 8)
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         float acc = 0.f;
+        if (mode == 21) {  // MUFU-heavy helpers (softmax exp phase stand-in)
+            float x = (float)threadIdx.x * 1e-3f;
+            while (!done) {
+#pragma unroll 16
+                for (int i = 0; i < 64; ++i) x = fast_exp2(x) * 0.5f;
+                acc += x;
+            }
+        } else
         while (!done) {
             for (int t = 0; t < 2; ++t) {
                 float v[32];
@@ -61,6 +69,7 @@ __global__ void __launch_bounds__(256, 1) probe(int mode, int iters, long long* 
         const uint32_t idS = idesc_bf16(128, 128, 0), idO = idesc_bf16(128, 80, 1), idO64 = idesc_bf16(128, 64, 1),
                        idO16 = idesc_bf16(128, 16, 1);
         long long t0 = clock64();
+        if (mode == 21) mode = 20;
         if (mode >= 9) {
             const uint32_t idS256 = idesc_bf16(128, 256, 0);
             for (int it = 0; it < iters; ++it) {
@@ -110,6 +119,17 @@ __global__ void __launch_bounds__(256, 1) probe(int mode, int iters, long long* 
                         }
                     }
                 }
+                if (mode == 18 || mode == 20) {  // S N=112, 2 tiles interleaved, 5 k-steps
+                    const uint32_t idS112 = idesc_bf16(128, 112, 0);
+                    for (int k = 0; k < 5; ++k)
+                        for (int t = 0; t < 2; ++t)
+                            mma_ss(tmem + 112 * t, dq128 + ((32 * (k & 3)) >> 4), dk128 + ((32 * (k & 3)) >> 4), idS112, k > 0);
+                }
+                if (mode == 19 || mode == 20) {  // PV 7 k-steps, N=80, 2 tiles interleaved, P at 384/448
+                    for (int k = 0; k < 7; ++k)
+                        for (int t = 0; t < 2; ++t)
+                            mma_ts(tmem + 224 + 80 * t, tmem + 384 + 64 * t + 8 * k, dv + ((512 * k) >> 4), idO, 1);
+                }
                 if (mode == 12) {  // S of 4 accumulators (N = 64 each... here N=128 into 4 x 128 cols) interleaved
                     for (int k = 0; k < 5; ++k)
                         for (int t = 0; t < 4; ++t)
@@ -155,10 +175,10 @@ __global__ void __launch_bounds__(256, 1) probe(int mode, int iters, long long* 
 int main() {
     long long* d; cudaMalloc(&d, 8);
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    const char* names[] = {"S+PV(TS,N80) x2tiles", "S only (5 MMA N128)", "PV TS N80 only", "PV SS N80 only", "S K64 only (4 MMA)", "S + PV SS", "PV TS N64 SW128 + N16 SW32", "mode0 + TMEM ld traffic", "mode0 + TMEM ld+st traffic", "S 2 tiles interleaved", "PV 2 tiles interleaved", "S N=256 x5", "S 4 accumulators interleaved", "PV SS 2 tiles interleaved", "PV TS 4 acc interleaved", "S+PV(TS) 1:1 per tile", "S+PV(SS) 1:1 per tile", "S(1-t)+PV(t) TS interleave"};
+    const char* names[] = {"S+PV(TS,N80) x2tiles", "S only (5 MMA N128)", "PV TS N80 only", "PV SS N80 only", "S K64 only (4 MMA)", "S + PV SS", "PV TS N64 SW128 + N16 SW32", "mode0 + TMEM ld traffic", "mode0 + TMEM ld+st traffic", "S 2 tiles interleaved", "PV 2 tiles interleaved", "S N=256 x5", "S 4 accumulators interleaved", "PV SS 2 tiles interleaved", "PV TS 4 acc interleaved", "S+PV(TS) 1:1 per tile", "S+PV(SS) 1:1 per tile", "S(1-t)+PV(t) TS interleave", "S N112 2x interleaved", "PV 7 steps 2x interleaved", "S112 + PV7 (kernel order)", "same + MUFU helper warps"};
     // per round (2 tiles) ideal clocks at 4096 MAC/clk: S = 2*128*128*80/4096 = 640, PV = 640
-    const double ideal[] = {1280, 640, 640, 640, 512, 1280, 640, 1280, 1280, 640, 640, 640, 1280, 640, 1280, 1280, 1280, 1280};
-    for (int mode = 0; mode < 18; ++mode) {
+    const double ideal[] = {1280, 640, 640, 640, 512, 1280, 640, 1280, 1280, 640, 640, 640, 1280, 640, 1280, 1280, 1280, 1280, 560, 560, 1120, 1120};
+    for (int mode = 0; mode < 22; ++mode) {
         const int iters = 200;
         probe<<<148, 256, 200 * 1024>>>(mode, iters, d);
         cudaError_t e = cudaDeviceSynchronize();
