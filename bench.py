@@ -371,16 +371,17 @@ def main():
     }
     achieved = flop_sp / t_sp / 1e12
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01_attn_ncu_full.json")
+    prof = os.path.join(ROOT, "profiles", "r01_attn_fa_ncu_full.json")
     if os.path.exists(prof) and args.config == "C3":
         caps = json.load(open(prof))
         # ncu raw page reports dram__bytes_{read,write}.sum in Mbyte; per launch
-        traffic = statistics.mean(c["dram__bytes_read.sum"] + c["dram__bytes_write.sum"] for c in caps) * 1e6
+        traffic = statistics.mean(c["dram__bytes_read.sum"] + c["dram__bytes_write.sum"] for c in caps
+                                  if c.get("site", "spatial") == "spatial") * 1e6
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
-                "traffic_note": "DRAM bytes per launch from profiles/r01_attn_ncu_full.json (ncu --set full); "
+                "traffic_note": "DRAM bytes per launch from profiles/r01_attn_fa_ncu_full.json (ncu --set full); "
                                 "algorithmic bytes 8*E = 460 MB (Q,K,V read + O write, bf16)",
-                "kernel": "attn_tc_kernel (spatial)",
+                "kernel": "attn_fa_kernel (spatial)",
                 "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
                 "algorithmic_flops_per_launch": flop_sp}
     flops_pab, _ = video_flops(cfg, table, c["batch"])

@@ -6,22 +6,21 @@
 // (pkg/src/pab_engine/model.py:346-359, 376-385):
 //   logits = q k^T * (1/sqrt(dh)); p = softmax(logits) (max-shifted); out = p v
 //
-// CTA (384 threads, one persistent CTA per SM; a work item is two 128-row query tiles
-// of one (problem, head) that share every K/V tile):
-//   warps 0-3   softmax + epilogue of query tile 0, one thread per query row (= TMEM lane)
-//   warps 4-7   softmax + epilogue of query tile 1
-//   warp  8     MMA issuer (lane 0 issues every tcgen05.mma; warp 8 owns TMEM)
-//   warp  9     TMA producer (lane 0)
-//   warp  10    V fixer: writes 1.0 into the first padded V column (see row sums)
-//   warp  11    idle
+// CTA (one persistent CTA per SM; a work item is two 128-row query tiles of one
+// (problem, head) that share every K/V tile).  With PAB_FA_SPLIT = S (default 1):
+//   warps [0, 4S)     softmax + epilogue of query tile 0: warp w owns TMEM lane quarter
+//                     w % 4 (one thread per query row) and column part (w >> 2) % S of the
+//                     112 keys (S = 2: the two warps of a row exchange maxima through smem)
+//   warps [4S, 8S)    the same for query tile 1
+//   warp  8S          MMA issuer (one elected lane issues the tcgen05.mma groups; owns TMEM)
+//   warp  8S + 1      TMA producer (lane 0)
+//   warp  8S + 2      V fixer (writes 1.0 into the first padded V column, see row sums)
 //
 // TMEM (512 columns), KV tiles of 112 keys so that S, P and O of both tiles fit side by
 // side (no aliasing):  S_t [112t, 112t + 112),  O_t [224 + OC t, ...),  P_t [384 + 64t, +56).
 // Because P does not overwrite S, the MMA warp issues S(j+1) = Q K_{j+1}^T as soon as
 // the softmax has pulled S(j) into registers, i.e. while it is still exponentiating,
-// and PV(j) when P(j) is stored.  The two tiles run in phase, so the MMA warp issues
-// S_0/S_1 and PV_0/PV_1 with their K-steps interleaved: tcgen05 MMAs on one accumulator
-// serialise at ~80 cycles each, two independent accumulators keep the tensor pipe full.
+// and PV(j) when P(j) is stored: the tensor pipe works in the shadow of the softmax.
 //
 // Row sums: the V fixer stores 1.0 into V column dh (zero padding otherwise), so the
 // PV MMA accumulates sum_k P[r, k] into O[r, dh] -- the softmax does no row-sum
@@ -40,17 +39,23 @@ namespace fa {
 
 using namespace pab::tc;
 
-constexpr int kThreads = 384;
+#ifndef PAB_FA_SPLIT
+#define PAB_FA_SPLIT 1  // softmax warps per (tile, TMEM lane quarter): each owns kKv / SPLIT columns
+#endif
+constexpr int kSplit = PAB_FA_SPLIT;
+constexpr int kSoftmaxWarps = 8 * kSplit;
+constexpr int kThreads = 32 * (kSoftmaxWarps + 3);
 constexpr int kRows = 128;   // query rows per tile == TMEM lanes
 constexpr int kKv = 112;     // keys per KV tile
-constexpr int kMmaWarp = 8;
-constexpr int kTmaWarp = 9;
-constexpr int kFixWarp = 10;
+constexpr int kHalf = kKv / kSplit;  // score columns per softmax thread
+constexpr int kMmaWarp = kSoftmaxWarps;
+constexpr int kTmaWarp = kSoftmaxWarps + 1;
+constexpr int kFixWarp = kSoftmaxWarps + 2;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kSCol = 0, kPCol = 384;
 
 #ifndef PAB_FA_POLY_DIV
-#define PAB_FA_POLY_DIV 4   // one column pair in PAB_FA_POLY_DIV on the FMA pipe (0: MUFU only)
+#define PAB_FA_POLY_DIV 3   // one column pair in PAB_FA_POLY_DIV on the FMA pipe (0: MUFU only)
 #endif
 
 struct Params {
@@ -88,7 +93,8 @@ struct Geometry {
     static constexpr int kQ0 = 0;        // 2 item buffers x 2 tiles
     static constexpr int kK0 = 4 * kSlot;  // 3-stage K ring
     static constexpr int kV0 = 7 * kSlot;  // 3-stage V ring
-    static constexpr int kBar = 10 * kSlot;
+    static constexpr int kX0 = 10 * kSlot;                 // row-max exchange [2][2][2][128] f32
+    static constexpr int kBar = kX0 + 8 * kRows * 4;
     static constexpr int kSmem = kBar + 512 + 1024;  // + barriers + alignment slack
     static constexpr uint32_t kOCol0 = 224, kOStride = kOCols;
     static_assert(N128 * 16384 + N32 * 4096 <= kSlot && NV * 4096 <= kSlot, "operand slot");
@@ -98,7 +104,7 @@ struct Geometry {
 
 struct Bars {
     uint64_t q_full[2], q_empty[2], k_full[3], k_empty[3], v_full[3], v_ready[3], v_empty[3];
-    uint64_t s_full, s_free, p_full, o_done;
+    uint64_t s_full, s_free, p_full, o_done;  // shared by the two query tiles (they run in phase)
 };
 
 // single-thread tcgen05.mma issue (lane 0 of the MMA warp): descriptors are passed as
@@ -196,12 +202,35 @@ __device__ __forceinline__ void mma_group_pv7(uint32_t o0, uint32_t o1, uint32_t
         : "memory");
 }
 
+// wait for two mbarrier phases with both try_waits in flight together (the MMA warp's
+// serial latency per iteration is dominated by barrier round trips)
+__device__ __forceinline__ void mbar_wait2(uint64_t* a, uint32_t pa, uint64_t* b, uint32_t pb) {
+    asm volatile(
+        "{\n\t.reg .pred x, y;\n"
+        "W2_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 x, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 y, [%2], %3;\n\t"
+        "and.pred x, x, y;\n\t"
+        "@!x bra W2_%=;\n}" ::"r"(smem_u32(a)),
+        "r"(pa), "r"(smem_u32(b)), "r"(pb)
+        : "memory");
+}
+
 __device__ __forceinline__ float max3(float a, float b, float c) {
     float r;
     asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
     return r;
 }
 
+#define PAB_TMEM_ST4U(taddr, r)                                                                          \
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r[0]), "r"(r[1]), \
+                 "r"(r[2]), "r"(r[3])                                                                        \
+                 : "memory")
+#define PAB_TMEM_LD8(taddr, r)                                                                           \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                \
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]),     \
+                   "=f"(r[7])                                                                             \
+                 : "r"(taddr))
 #define PAB_TMEM_ST8U(taddr, r)                                                                          \
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), \
                  "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])  \
@@ -308,8 +337,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&bars->v_empty[s], 1);
         }
         mbar_init(&bars->s_full, 1);
-        mbar_init(&bars->s_free, 8);  // one arrival per softmax warp (both tiles)
-        mbar_init(&bars->p_full, 8);
+        mbar_init(&bars->s_free, kSoftmaxWarps);  // one arrival per softmax warp
+        mbar_init(&bars->p_full, kSoftmaxWarps);
         mbar_init(&bars->o_done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -325,17 +354,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the CTA allocates all 512 columns, so the TMEM base address is lane 0 / column 0
     constexpr uint32_t tmem = 0;
 
-    if (warp < 8) {
+    if (warp < kSoftmaxWarps) {
         // ========================================= softmax + epilogue of query tile t
-        const int t = warp >> 2;
+        // warp = 8 t + 4 h + quarter: TMEM lane quarter = warp % 4 (the tcgen05.ld/st lane
+        // restriction), column half h of the 112-key S tile
+        const int t = warp / (4 * kSplit);
+        const int hc = (warp >> 2) % kSplit;
         const int wl = warp & 3;
         const int row = wl * 32 + lane;
         const uint32_t lane_off = (uint32_t)(wl * 32) << 16;
-        const uint32_t s_tmem = tmem + lane_off + kSCol + kKv * t;
+        const uint32_t s_tmem = tmem + lane_off + kSCol + kKv * t + kHalf * hc;
         const uint32_t o_tmem = tmem + lane_off + G::kOCol0 + G::kOStride * t;
-        const uint32_t p_tmem = tmem + lane_off + kPCol + 64 * t;
-        const int tail = p.n_k - (n_kv - 1) * kKv;  // live keys of the last KV tile
-        const bool trc = (wl == 0 && lane == 0);
+        const uint32_t p_tmem = tmem + lane_off + kPCol + 64 * t + (kHalf / 2) * hc;
+        const int tail = p.n_k - (n_kv - 1) * kKv - kHalf * hc;  // live keys of the last KV tile in this half
+        const bool trc = (wl == 0 && lane == 0 && hc == 0);
+        // O chunks (16 columns) this half rescales / stores
+        constexpr int kOHalf = (kSplit == 1) ? NV : (NV + 1) / 2;
+        const int oc_lo = hc ? kOHalf : 0, oc_hi = hc ? NV : kOHalf;
+        // row max exchange with the other column half: [parity][tile][half][row]
+        float* xch = reinterpret_cast<float*>(smem + G::kX0);
+        const uint32_t xbar = 1 + 4 * t + wl;  // named barrier of the two warps sharing these rows
         // O of the previous item of this tile -> normalised bf16 rows (its last P.V done)
         auto epilogue = [&](const Item& it) {
             float o[16];
@@ -349,8 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool store = i < p.n_q;
             __nv_bfloat16* dst = p.o + (int64_t)it.a_idx * p.o_sa + (int64_t)it.b_idx * p.o_sb + (int64_t)i * p.o_si +
                                  (int64_t)it.h * p.dh;
-#pragma unroll
-            for (int cc = 0; cc < NV; ++cc) {
+            for (int cc = oc_lo; cc < oc_hi; ++cc) {
                 if (16 * cc >= p.dh) break;
                 PAB_TMEM_LD16(o_tmem + 16 * cc, o);
                 tmem_wait_ld();
@@ -369,65 +406,84 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         Item prev;
         bool have_prev = false;
-        int gi = 0;
+        int it_n = 0;  // iterations of this tile (tile 1 skips single-tile items)
         for (int c = 0; c < my_items; ++c) {
             const Item it = decode((int)blockIdx.x + c * (int)gridDim.x);
             const bool active = (t == 0) || it.two;
             float m_run = -INFINITY;
-            for (int j = 0; j < n_kv; ++j, ++gi) {
-                FA_TRACE(trc, gi, t, 0);
-                mbar_wait(&bars->s_full, gi & 1);
+            for (int j = 0; j < n_kv; ++j, ++it_n) {
+                FA_TRACE(trc, it_n, t, 0);
+                mbar_wait(&bars->s_full, it_n & 1);
                 tc_fence_after();
-                FA_TRACE(trc, gi, t, 1);
-                if (!active) {
-                    // second tile absent: arrive on the pair's barriers with the same waits as
-                    // an active tile (o_done(gi - 1) before p_full(gi)), so these arrivals can
-                    // never run a phase ahead of tile 0's and complete a phase on their own
+                FA_TRACE(trc, it_n, t, 1);
+                float s[kHalf];
+#ifndef PAB_FA_DIAG_BARRIERS_ONLY  // timing diagnostic only: the barrier protocol without softmax work
+                if (!active)
+#endif
+                {
+                    // second tile absent: arrive on the pair's barriers with the same waits as an
+                    // active tile (o_done(gi - 1) before p_full(gi)), so these arrivals can never
+                    // run a phase ahead and complete a phase on their own
+                    tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&bars->s_free);
-                    if (gi > 0) mbar_wait(&bars->o_done, (gi - 1) & 1);
+                    if (it_n > 0) mbar_wait(&bars->o_done, (it_n - 1) & 1);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&bars->p_full);
                     continue;
                 }
-                float s[kKv];
-                PAB_TMEM_LD32(s_tmem, s);
-                PAB_TMEM_LD32(s_tmem + 32, (s + 32));
-                PAB_TMEM_LD32(s_tmem + 64, (s + 64));
-                PAB_TMEM_LD16(s_tmem + 96, (s + 96));
+                if (kSplit == 1) {
+                    PAB_TMEM_LD32(s_tmem, s);
+                    PAB_TMEM_LD32(s_tmem + 32, (s + 32));
+                    PAB_TMEM_LD32(s_tmem + 64, (s + 64));
+                    PAB_TMEM_LD16(s_tmem + 96, (s + 96));
+                } else {
+                    PAB_TMEM_LD32(s_tmem, s);
+                    PAB_TMEM_LD16(s_tmem + 32, (s + 32));
+                    PAB_TMEM_LD8(s_tmem + 48, (s + 48));
+                }
                 tmem_wait_ld();
-                // S is in registers: the MMA warp may overwrite it with S(j+1)
+                // S is in registers: the MMA warp may overwrite it with the next S
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->s_free);
-                FA_TRACE(trc, gi, t, 2);
-                const bool masked = (j == n_kv - 1) && (tail < kKv);
+                FA_TRACE(trc, it_n, t, 2);
+                const bool masked = (j == n_kv - 1) && (tail < kHalf);
                 if (masked) {
 #pragma unroll
-                    for (int cc = 0; cc < kKv; ++cc) s[cc] = (cc < tail) ? s[cc] : -INFINITY;
+                    for (int cc = 0; cc < kHalf; ++cc) s[cc] = (cc < tail) ? s[cc] : -INFINITY;
                 }
-                // row max of the raw scores (scale > 0 commutes with max)
+                // row max of the raw scores (scale > 0 commutes with max), then with the other half
+                constexpr int kG = kHalf / 4;  // 4 independent FMNMX3 chains
                 float m4[4];
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
-                    float m = fmaxf(s[28 * g], s[28 * g + 1]);
+                    float m = s[kG * g];
 #pragma unroll
-                    for (int cc = 2; cc < 28; cc += 2) m = max3(m, s[28 * g + cc], s[28 * g + cc + 1]);
-                    m4[g] = m;
+                    for (int cc = 1; cc + 1 < kG; cc += 2) m = max3(m, s[kG * g + cc], s[kG * g + cc + 1]);
+                    m4[g] = (kG % 2 == 0) ? fmaxf(m, s[kG * g + kG - 1]) : m;
                 }
-                const float m_tile = max3(fmaxf(m4[0], m4[1]), m4[2], m4[3]) * p.scale_log2;
+                float mx = max3(fmaxf(m4[0], m4[1]), m4[2], m4[3]);
+                if (kSplit > 1) {
+                    float* xs = xch + ((it_n & 1) * 2 + t) * 2 * kRows;
+                    xs[hc * kRows + row] = mx;
+                    asm volatile("bar.sync %0, %1;" ::"r"(xbar), "r"(64) : "memory");
+                    mx = fmaxf(mx, xs[(1 - hc) * kRows + row]);
+                }
+                const float m_tile = mx * p.scale_log2;
+                // both halves hold identical (m_tile, m_run) per row and take the same decisions
                 const bool need = m_tile > m_run + 8.0f;
-                // PV(gi - 1) must be complete before O is rescaled or P is overwritten
+                // the previous P.V of this tile must be complete before O is rescaled or P overwritten
                 bool waited = false;
                 if (__any_sync(0xffffffffu, need)) {
                     const float m_new = need ? m_tile : m_run;
                     if (j > 0) {
-                        mbar_wait(&bars->o_done, (gi - 1) & 1);
+                        mbar_wait(&bars->o_done, (it_n - 1) & 1);
                         tc_fence_after();
                         waited = true;
                         const float alpha = fast_exp2(m_run - m_new);
 #pragma unroll 1
-                        for (int cc = 0; cc < NV; ++cc) {
+                        for (int cc = oc_lo; cc < oc_hi; ++cc) {
                             float o[16];
                             PAB_TMEM_LD16(o_tmem + 16 * cc, o);
                             tmem_wait_ld();
@@ -438,36 +494,52 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     m_run = m_new;
                 }
-                FA_TRACE(trc, gi, t, 3);
+                FA_TRACE(trc, it_n, t, 3);
                 const float neg_m = -m_run;
                 const unsigned long long sc2 = f2_pack(p.scale_log2, p.scale_log2), nm2 = f2_pack(neg_m, neg_m);
-                uint32_t pk[kKv / 2];
-                if (masked) {
-                    exp_pack<true, 16>(s, 0, sc2, nm2, tail, pk);
-                    exp_pack<true, 16>(s, 32, sc2, nm2, tail, pk + 16);
-                    exp_pack<true, 16>(s, 64, sc2, nm2, tail, pk + 32);
-                    exp_pack<true, 8>(s, 96, sc2, nm2, tail, pk + 48);
+                uint32_t pk[kHalf / 2];
+                if (kSplit == 1) {
+                    if (masked) {
+                        exp_pack<true, 16>(s, 0, sc2, nm2, tail, pk);
+                        exp_pack<true, 16>(s, 32, sc2, nm2, tail, pk + 16);
+                        exp_pack<true, 16>(s, 64, sc2, nm2, tail, pk + 32);
+                        exp_pack<true, 8>(s, 96, sc2, nm2, tail, pk + 48);
+                    } else {
+                        exp_pack<false, 16>(s, 0, sc2, nm2, kHalf, pk);
+                        exp_pack<false, 16>(s, 32, sc2, nm2, kHalf, pk + 16);
+                        exp_pack<false, 16>(s, 64, sc2, nm2, kHalf, pk + 32);
+                        exp_pack<false, 8>(s, 96, sc2, nm2, kHalf, pk + 48);
+                    }
                 } else {
-                    exp_pack<false, 16>(s, 0, sc2, nm2, kKv, pk);
-                    exp_pack<false, 16>(s, 32, sc2, nm2, kKv, pk + 16);
-                    exp_pack<false, 16>(s, 64, sc2, nm2, kKv, pk + 32);
-                    exp_pack<false, 8>(s, 96, sc2, nm2, kKv, pk + 48);
+                    if (masked) {
+                        exp_pack<true, 16>(s, 0, sc2, nm2, tail, pk);
+                        exp_pack<true, 12>(s, 32, sc2, nm2, tail, pk + 16);
+                    } else {
+                        exp_pack<false, 16>(s, 0, sc2, nm2, kHalf, pk);
+                        exp_pack<false, 12>(s, 32, sc2, nm2, kHalf, pk + 16);
+                    }
                 }
-                FA_TRACE(trc, gi, t, 4);
-                if (!waited && gi > 0) {
-                    mbar_wait(&bars->o_done, (gi - 1) & 1);
+                FA_TRACE(trc, it_n, t, 4);
+                if (!waited && it_n > 0) {
+                    mbar_wait(&bars->o_done, (it_n - 1) & 1);
                     tc_fence_after();
                 }
                 if (j == 0 && have_prev) epilogue(prev);  // O of the previous item is final
-                PAB_TMEM_ST16U(p_tmem, pk);
-                PAB_TMEM_ST16U(p_tmem + 16, (pk + 16));
-                PAB_TMEM_ST16U(p_tmem + 32, (pk + 32));
-                PAB_TMEM_ST8U(p_tmem + 48, (pk + 48));
+                if (kSplit == 1) {
+                    PAB_TMEM_ST16U(p_tmem, pk);
+                    PAB_TMEM_ST16U(p_tmem + 16, (pk + 16));
+                    PAB_TMEM_ST16U(p_tmem + 32, (pk + 32));
+                    PAB_TMEM_ST8U(p_tmem + 48, (pk + 48));
+                } else {
+                    PAB_TMEM_ST16U(p_tmem, pk);
+                    PAB_TMEM_ST8U(p_tmem + 16, (pk + 16));
+                    PAB_TMEM_ST4U(p_tmem + 24, (pk + 24));
+                }
                 tmem_wait_st();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->p_full);
-                FA_TRACE(trc, gi, t, 5);
+                FA_TRACE(trc, it_n, t, 5);
             }
             if (active) {
                 prev = it;
@@ -475,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         if (have_prev) {
-            mbar_wait(&bars->o_done, (n_iters - 1) & 1);
+            mbar_wait(&bars->o_done, (it_n - 1) & 1);
             tc_fence_after();
             epilogue(prev);
         }
@@ -525,18 +597,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == kFixWarp) {
         // ====================================== V fixer: V[:, dh] = 1 (zero-filled by TMA)
-        // SW32 atom layout: row r at 32 r, 16-byte chunk index XOR (r >> 2) & 1
+        // the P.V MMA then accumulates the row sums into O[:, dh].
+        // SW32 atom layout: row r at 32 r, 16-byte chunk index XOR (r >> 2) & 1.
         const int col = p.dh % 16;
         const uint32_t atom_off = (uint32_t)(p.dh / 16) * 4096u;
         for (int g = 0; g < n_iters; ++g) {
             const int st = g % 3;
             mbar_wait(&bars->v_full[st], (g / 3) & 1);
             uint8_t* vd = smem + G::kV0 + st * G::kSlot + atom_off;
-#pragma unroll
             for (int r = lane; r < kKv; r += 32) {
                 const uint32_t chunk = (uint32_t)(col >> 3) ^ (uint32_t)((r >> 2) & 1);
-                *reinterpret_cast<__nv_bfloat16*>(vd + r * 32 + chunk * 16 + (col & 7) * 2) =
-                    __float2bfloat16_rn(1.0f);
+                *reinterpret_cast<__nv_bfloat16*>(vd + r * 32 + chunk * 16 + (col & 7) * 2) = __float2bfloat16_rn(1.0f);
             }
             fence_async_smem();
             __syncwarp();
@@ -559,65 +630,60 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int n = min(kKv, p.n_k - j * kKv);
             return (n + 15) & ~15;
         };
-        // S_t = Q_t K^T for the active tiles, K-steps interleaved across the two accumulators
-        auto issue_s = [&](int qb, int kst, int ncols, int nt) {
+        // S_t = Q_t K^T for the item's tiles (Q slots 2 qb + t, K stage kst), K-steps of the
+        // two tiles interleaved: MMAs on one accumulator serialise at ~80 cycles each, two
+        // independent accumulators keep the tensor pipe busy.  ncols = keys rounded up to 16.
+        auto issue_s = [&](int qb, int kst, int ncols, bool two) {
             const uint32_t ka = k_lo + ((kst * G::kSlot) >> 4);
+            const uint32_t qa0 = q_lo + ((2 * qb * G::kSlot) >> 4);
             const uint32_t idS = (idS128 & ~(0x3Fu << 17)) | ((uint32_t)(ncols >> 3) << 17);
             if (N128 == 1 && N32 == 1) {
-                const uint32_t qa = q_lo + ((2 * qb * G::kSlot) >> 4);
-                const uint64_t dq = ((uint64_t)kHi128 << 32) | (qa | kLbo16), dk = ((uint64_t)kHi128 << 32) | (ka | kLbo16);
-                const uint64_t dq32 = ((uint64_t)kHi32 << 32) | ((qa + (16384 >> 4)) | kLbo16);
+                const uint64_t dq = ((uint64_t)kHi128 << 32) | (qa0 | kLbo16);
+                const uint64_t dk = ((uint64_t)kHi128 << 32) | (ka | kLbo16);
+                const uint64_t dq32 = ((uint64_t)kHi32 << 32) | ((qa0 + (16384 >> 4)) | kLbo16);
                 const uint64_t dk32 = ((uint64_t)kHi32 << 32) | ((ka + (16384 >> 4)) | kLbo16);
-                mma_group_s_72(tmem + kSCol, tmem + kSCol + kKv, dq, dk, dq32, dk32, idS, nt == 2, G::kSlot >> 4);
+                mma_group_s_72(tmem + kSCol, tmem + kSCol + kKv, dq, dk, dq32, dk32, idS, two, G::kSlot >> 4);
                 return;
             }
             if (lane != 0) return;
-#pragma unroll
-            for (int blk = 0; blk < N128; ++blk)
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t o = (blk * 16384 + 32 * k) >> 4;
-                    for (int t = 0; t < nt; ++t) {
-                        const uint32_t qa = q_lo + (((2 * qb + t) * G::kSlot) >> 4);
-                        mma_ss1(tmem + kSCol + kKv * t, (qa + o) | kLbo16, kHi128, (ka + o) | kLbo16, kHi128, idS,
-                                (blk | k) != 0);
+            for (int t = 0; t < (two ? 2 : 1); ++t) {
+                const uint32_t qa = qa0 + ((t * G::kSlot) >> 4);
+                const uint32_t d_s = tmem + kSCol + kKv * t;
+                for (int blk = 0; blk < N128; ++blk)
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t o = (blk * 16384 + 32 * k) >> 4;
+                        mma_ss1(d_s, (qa + o) | kLbo16, kHi128, (ka + o) | kLbo16, kHi128, idS, (blk | k) != 0);
                     }
-                }
-#pragma unroll
-            for (int blk = 0; blk < N32; ++blk) {
-                const uint32_t o = (N128 * 16384 + blk * 4096) >> 4;
-                for (int t = 0; t < nt; ++t) {
-                    const uint32_t qa = q_lo + (((2 * qb + t) * G::kSlot) >> 4);
-                    mma_ss1(tmem + kSCol + kKv * t, (qa + o) | kLbo16, kHi32, (ka + o) | kLbo16, kHi32, idS,
-                            (N128 | blk) != 0);
+                for (int blk = 0; blk < N32; ++blk) {
+                    const uint32_t o = (N128 * 16384 + blk * 4096) >> 4;
+                    mma_ss1(d_s, (qa + o) | kLbo16, kHi32, (ka + o) | kLbo16, kHi32, idS, (N128 | blk) != 0);
                 }
             }
         };
-        // O_t += P_t V: ncols / 16 K-steps of 16 keys; A = P_t from TMEM (8 columns per step)
-        auto issue_pv = [&](int vst, uint32_t accumulate, int ncols, int nt) {
+        // O_t += P_t V: ncols / 16 K-steps of 16 keys, both tiles interleaved; A = P_t from TMEM
+        auto issue_pv = [&](int vst, uint32_t accumulate, int ncols, bool two) {
             const uint32_t va = v_lo + ((vst * G::kSlot) >> 4);
             if (kKv / 16 == 7) {
                 const uint64_t dv = ((uint64_t)kHi32 << 32) | (va | kLboV);
-                mma_group_pv7(tmem + G::kOCol0, tmem + G::kOCol0 + G::kOStride, tmem + kPCol, tmem + kPCol + 64, dv, idO,
-                              accumulate, nt == 2, ncols / 16);
+                mma_group_pv7(tmem + G::kOCol0, tmem + G::kOCol0 + G::kOStride, tmem + kPCol, tmem + kPCol + 64, dv,
+                              idO, accumulate, two, ncols / 16);
                 return;
             }
             if (lane != 0) return;
             for (int k = 0; 16 * k < ncols; ++k)
-                for (int t = 0; t < nt; ++t)
+                for (int t = 0; t < (two ? 2 : 1); ++t)
                     mma_ts1(tmem + G::kOCol0 + G::kOStride * t, tmem + kPCol + 64 * t + 8 * k,
                             (va + ((512 * k) >> 4)) | kLboV, kHi32, idO, accumulate | (k > 0));
         };
-        // iteration gi = (item c, kv tile j); S(gi + 1) is issued as soon as the softmax has
-        // read S(gi), PV(gi) when P(gi) is stored
+        // iteration gi = (item c, kv tile j), KV tile g.  The tiles run in phase: S(gi+1) of
+        // both tiles is issued once both softmaxes have read S(gi) (early in their iteration),
+        // PV(gi) once both have stored P(gi).
         int c = 0, j = 0, g = 0;
         Item it = decode((int)blockIdx.x);
-        int nt = it.two ? 2 : 1;
         if (my_items > 0) {
-            mbar_wait(&bars->q_full[0], 0);
-            mbar_wait(&bars->k_full[0], 0);
+            mbar_wait2(&bars->q_full[0], 0, &bars->k_full[0], 0);
             tc_fence_after();
-            issue_s(0, 0, cols_of(0), nt);
+            issue_s(0, 0, cols_of(0), it.two);
             tc_commit(&bars->s_full);
             tc_commit(&bars->k_empty[0]);
             if (n_kv == 1) tc_commit(&bars->q_empty[0]);
@@ -633,23 +699,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const Item it1 = (c1 == c) ? it : decode((int)blockIdx.x + c1 * (int)gridDim.x);
                 const int g1 = g + 1;
                 FA_TRACE(lane == 0, gi, 0, 10);
-                mbar_wait(&bars->s_free, gi & 1);
                 if (j1 == 0) mbar_wait(&bars->q_full[c1 & 1], (c1 >> 1) & 1);
-                mbar_wait(&bars->k_full[g1 % 3], (g1 / 3) & 1);
+                mbar_wait2(&bars->s_free, gi & 1, &bars->k_full[g1 % 3], (g1 / 3) & 1);
                 tc_fence_after();
                 FA_TRACE(lane == 0, gi, 0, 8);
-                issue_s(c1 & 1, g1 % 3, cols_of(j1), it1.two ? 2 : 1);
+                issue_s(c1 & 1, g1 % 3, cols_of(j1), it1.two);
                 tc_commit(&bars->s_full);
                 tc_commit(&bars->k_empty[g1 % 3]);
                 if (j1 == n_kv - 1) tc_commit(&bars->q_empty[c1 & 1]);  // last S of item c1 issued
             }
             // ---- PV of this iteration
             FA_TRACE(lane == 0, gi, 1, 10);
-            mbar_wait(&bars->p_full, gi & 1);
-            mbar_wait(&bars->v_ready[g % 3], (g / 3) & 1);
+            mbar_wait2(&bars->p_full, gi & 1, &bars->v_ready[g % 3], (g / 3) & 1);
             tc_fence_after();
             FA_TRACE(lane == 0, gi, 1, 8);
-            issue_pv(g % 3, j > 0, cols_of(j), nt);
+            issue_pv(g % 3, j > 0, cols_of(j), it.two);
             tc_commit(&bars->o_done);
             tc_commit(&bars->v_empty[g % 3]);
             FA_TRACE(lane == 0, gi, 1, 9);
@@ -657,10 +721,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (++j == n_kv) {
                 j = 0;
                 ++c;
-                if (c < my_items) {
-                    it = decode((int)blockIdx.x + c * (int)gridDim.x);
-                    nt = it.two ? 2 : 1;
-                }
+                if (c < my_items) it = decode((int)blockIdx.x + c * (int)gridDim.x);
             }
         }
     }
