@@ -21,6 +21,14 @@ a rank of a torch.distributed NCCL group on its own B200:
 The communication ledger records one entry per reshard with the reference's
 element count B*T*S*D*(W-1)/W (parallel.py:130-133, 167-179), so the
 executed event count equals 2 * L * |temporal compute steps|.
+
+``split_batch`` (reference parallel.py:410-464): with guidance on an even
+number of ranks, ranks [0, W/2) run the conditional half and [W/2, W) the
+unconditional half, each half frame-sharded over its own W/2-rank group.
+After every step the two ranks holding the same frames exchange their eps
+(one all-gather over a 2-rank group) and both apply the same fused
+CFG + DDIM update, so the halves stay in lock step exactly as the
+reference's shared eps_hat.
 """
 
 from __future__ import annotations
@@ -214,6 +222,17 @@ def _all_gather(t, group=None):
     return parts
 
 
+def _all_gather_into(out, t, group=None):
+    """out (world, *t.shape) <- t of every rank of `group`, in group-rank order."""
+    import torch.distributed as dist
+
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        for dst, part in zip(out, _all_gather(t.contiguous(), group)):
+            dst.copy_(part.view_as(dst))
+        return
+    dist.all_gather_into_tensor(out.view(-1), t.contiguous().view(-1), group=group)
+
+
 def exchange_frames_to_tokens(send, recv, group=None):
     """send: (W, T/W, B, S/W, D) by destination -> recv: (W_src, T/W, B, S/W, D)
     = (T, B, S/W, D) token layout (frame index = src * T/W + t)."""
@@ -235,7 +254,7 @@ def unpack_frames(recv, out):
 class _SPTemporal:
     """Token-layout workspaces + the temporal-site hook for run_forward."""
 
-    def __init__(self, ctx, world: int, group, ledger: CommReport, bytes_per_element: int):
+    def __init__(self, ctx, world: int, group, ledger: CommReport, bytes_per_element: int, groups: int = 1):
         import torch
 
         from . import kernels
@@ -261,6 +280,7 @@ class _SPTemporal:
                                       ctx.H, ctx.dh)
         self.el = _alltoall_elements(B, ctx.cfg, world)
         self.wire = Tl * B * Sw * D * 2 * (world - 1)
+        self.groups = groups  # split_batch: the job-wide ledger holds one entry per rank group
         self.bpe = bytes_per_element
 
     def __call__(self, st, li, lp):
@@ -306,8 +326,9 @@ class _SPTemporal:
         st.record(li, TM, "t", decision, source, o)
 
     def _log(self, step, layer):
-        self.ledger.entries.append(CommEntry(step, layer, self.ledger.method, self.el, self.el * self.bpe,
-                                             self.el > 0, self.wire))
+        for _ in range(self.groups):
+            self.ledger.entries.append(CommEntry(step, layer, self.ledger.method, self.el, self.el * self.bpe,
+                                                 self.el > 0, self.wire))
 
 
 class ShardedDenoiser:
@@ -315,26 +336,39 @@ class ShardedDenoiser:
 
     def __init__(self, params: ModelParams, schedule, table: DecisionTable, text_ids, *, guidance: bool,
                  guidance_scale: float, rank: int, world: int, group=None, method: str = "broadcast_sp",
-                 noise_params: NoiseParams = DEFAULT_NOISE, bytes_per_element: int = 4, trace=None):
+                 noise_params: NoiseParams = DEFAULT_NOISE, bytes_per_element: int = 4, trace=None,
+                 half: Optional[int] = None, cfg_group=None, total_workers: Optional[int] = None):
+        """rank/world/group: this rank's position in its sequence-parallel group.
+        split_batch: half = 0 (conditional) / 1 (unconditional) CFG half run by this
+        group, cfg_group = the 2-rank group {cond rank, uncond rank} of these frames."""
         from .runtime import StepContext
 
         cfg = params.cfg
         self.plan = plan_shards(world, cfg)
         self.params, self.table, self.rank, self.world, self.group = params, table, rank, world, group
         self.guidance, self.g = bool(guidance), float(guidance_scale)
-        self.batch = 2 if guidance else 1
+        self.half, self.cfg_group = half, cfg_group
+        split = half is not None
+        if split and not guidance:
+            raise ValidationError("split_batch needs classifier-free guidance")
+        self.batch = 1 if split else (2 if guidance else 1)
         ids = np.asarray(text_ids, dtype=np.int64)
-        self.ids = np.stack([ids, np.full_like(ids, -1)]) if guidance else ids[None, :]
+        if split:
+            self.ids = (ids if half == 0 else np.full_like(ids, -1))[None, :]
+        else:
+            self.ids = np.stack([ids, np.full_like(ids, -1)]) if guidance else ids[None, :]
         ts = list(getattr(schedule, "timesteps", schedule))
         self.timesteps = ts
         self.alphas = [(noise_params.alpha_bar(t), noise_params.alpha_bar(ts[i + 1]) if i + 1 < len(ts) else 1.0)
                        for i, t in enumerate(ts)]
         self.ctx = StepContext.build(params, self.batch, self.ids, ts, frames=self.plan.frames_per_worker)
-        self.ledger = CommReport(method, world, bytes_per_element, METHOD_COSTS[method])
-        self.hook = _SPTemporal(self.ctx, world, group, self.ledger, bytes_per_element) if world > 1 else None
+        self.ledger = CommReport(method, total_workers or world, bytes_per_element, METHOD_COSTS[method])
+        self.hook = (_SPTemporal(self.ctx, world, group, self.ledger, bytes_per_element, 2 if split else 1)
+                     if world > 1 else None)
         self.cache = CacheStore()
         self.trace = trace
         self._r = None
+        self._pair = None
 
     def shard_input(self, x_full):
         """This rank's frames of a full (B, T, S, D) latent (contiguous copy)."""
@@ -348,25 +382,68 @@ class ShardedDenoiser:
 
         if self._r is None or self._r.shape != z.shape:
             self._r = torch.empty_like(z)
+        split = self.half is not None
+        if split and (self._pair is None or self._pair[0].shape[1:] != z.shape[1:]):
+            # (2, T/W, S, D) pair buffers: eps of both halves, latent slot per half
+            self._pair = (torch.empty((2, *z.shape[1:]), device=z.device, dtype=z.dtype),
+                          torch.empty((2, *z.shape[1:]), device=z.device, dtype=z.dtype))
         for i, t in enumerate(self.timesteps):
             a_cur, a_next = self.alphas[i]
-            run_forward(self.ctx, i, t, z, self._r, self.table.slice(i), self.cache, trace=self.trace,
-                        finish="ddim", ddim=(self.guidance, self.g, a_cur, a_next), temporal_hook=self.hook)
+            if not split:
+                run_forward(self.ctx, i, t, z, self._r, self.table.slice(i), self.cache, trace=self.trace,
+                            finish="ddim", ddim=(self.guidance, self.g, a_cur, a_next), temporal_hook=self.hook)
+            else:
+                # eps of this half -> exchange with the partner rank -> the shared CFG + DDIM update
+                # (reference parallel.py:446-457: eps_hat = eps_u + g (eps_c - eps_u) for both halves)
+                run_forward(self.ctx, i, t, z, self._r, self.table.slice(i), self.cache, trace=self.trace,
+                            finish="residual", temporal_hook=self.hook)
+                eps2, z2 = self._pair
+                _all_gather_into(eps2, self._r, self.cfg_group)
+                z2[self.half].copy_(z[0])
+                z2[1 - self.half].copy_(z[0])
+                from . import kernels
+
+                kernels.ddim_cfg(z2, eps2, [], True, self.g, a_cur, a_next)
+                self.ctx.launches.other_calls += 1
+                z[0].copy_(z2[self.half])
             if on_step is not None:
                 on_step(i, z)
         return z
 
     def __call__(self, x_host, out=None):
-        """Serving call on this rank: H2D of its frames of the pinned host
-        latent, denoise, D2H of its frames into `out` (or a new tensor)."""
+        """Serving call on this rank: H2D of its frames (of its CFG half under
+        split_batch) of the pinned host latent, denoise, D2H into `out` (or a new tensor)."""
         n = self.plan.frames_per_worker
         sl = slice(self.rank * n, (self.rank + 1) * n)
-        z = x_host[:, sl].to(self.params.w_time.device, non_blocking=True)
+        bl = slice(None) if self.half is None else slice(self.half, self.half + 1)
+        z = x_host[bl, sl].to(self.params.w_time.device, non_blocking=True)
         self.run(z)
         if out is None:
             return z.cpu()
-        out[:, sl].copy_(z, non_blocking=True)
+        out[bl, sl].copy_(z, non_blocking=True)
         return out
+
+
+def split_batch_denoiser(params: ModelParams, schedule, table: DecisionTable, text_ids, *, guidance_scale: float,
+                         method: str = "broadcast_sp", noise_params: NoiseParams = DEFAULT_NOISE,
+                         bytes_per_element: int = 4, trace=None) -> "ShardedDenoiser":
+    """Collective (every rank calls it): CFG halves on two rank groups of W/2
+    (reference parallel.py:410-434).  Ranks [0, W/2) run the conditional half,
+    [W/2, W) the unconditional one; rank w and W/2 + w hold the same frames."""
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(), dist.get_rank()
+    if world < 2 or world % 2:
+        raise ValidationError("split_batch needs an even number of ranks")
+    gw = world // 2
+    # new_group is collective over the default group: every rank creates every group, same order
+    sp = [dist.new_group(list(range(g * gw, (g + 1) * gw))) for g in range(2)]
+    pairs = [dist.new_group([w, gw + w]) for w in range(gw)]
+    half, w = divmod(rank, gw)
+    return ShardedDenoiser(params, schedule, table, text_ids, guidance=True, guidance_scale=guidance_scale,
+                           rank=w, world=gw, group=sp[half], method=method, noise_params=noise_params,
+                           bytes_per_element=bytes_per_element, trace=trace, half=half, cfg_group=pairs[w],
+                           total_workers=world)
 
 
 @dataclass
@@ -385,19 +462,26 @@ class ParallelRunResult:
         if not self.worker_caches:
             return merged
         local = self.worker_caches[0]
-        world = self.plan.workers
         import torch.distributed as dist
 
-        multi = dist.is_available() and dist.is_initialized() and world > 1
+        multi = dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+        from .runtime import canonical
+
         for site, entry in sorted(local.entries.items(), key=lambda kv: str(kv[0])):
-            v = entry.value
+            # a rank group of one runs the serial temporal site, whose cache is token-major
+            v = canonical(entry.value, (self._batch, self.plan.frames_per_worker, self._tail[0])).contiguous()
             if multi:
                 parts = _all_gather(v.contiguous())
             else:
                 parts = [c.entries[site].value for c in self.worker_caches]
             B = self._batch
             parts = [p.reshape(B, -1, *self._tail) for p in parts]
-            merged[site] = torch.cat(parts, dim=1).float().cpu().numpy()
+            gw = getattr(self, "_split_gw", None)
+            if gw:  # split_batch: frames within a rank group, CFG halves across the two groups
+                full = torch.cat([torch.cat(parts[:gw], dim=1), torch.cat(parts[gw:], dim=1)], dim=0)
+            else:
+                full = torch.cat(parts, dim=1)
+            merged[site] = full.float().cpu().numpy()
         return merged
 
 
@@ -433,8 +517,6 @@ def run_parallel(
         raise ValidationError(f"method {method!r} is not executable; use comm_volume_model for it")
     if method == "broadcast_sp" and not isinstance(policy, PabPolicy):
         raise ValidationError("broadcast_sp requires a PAB policy")
-    if split_batch and guidance and workers >= 2 and workers % 2 == 0:
-        raise ValidationError("split_batch (CFG halves on separate rank groups) is not implemented yet")
     if table is None:
         table = build_schedule(policy, schedule, cfg.layers, range_semantics=range_semantics)
     if text_ids is None:
@@ -445,18 +527,32 @@ def run_parallel(
     if workers != world:
         raise ValidationError(f"run_parallel(workers={workers}) must run in a process group of that size "
                               f"(got world size {world}); launch with torchrun --nproc-per-node {workers}")
-    den = ShardedDenoiser(params, schedule, table, text_ids, guidance=guidance, guidance_scale=guidance_scale,
-                          rank=rank, world=world, method=method, noise_params=noise_params,
-                          bytes_per_element=bytes_per_element)
-    x_full = torch.from_numpy(initial_latent(params, seed, den.batch)).to(params.w_time.device)
+    use_split = bool(split_batch and guidance and workers >= 2 and workers % 2 == 0)
+    if use_split:
+        den = split_batch_denoiser(params, schedule, table, text_ids, guidance_scale=guidance_scale,
+                                   method=method, noise_params=noise_params, bytes_per_element=bytes_per_element)
+    else:
+        den = ShardedDenoiser(params, schedule, table, text_ids, guidance=guidance, guidance_scale=guidance_scale,
+                              rank=rank, world=world, method=method, noise_params=noise_params,
+                              bytes_per_element=bytes_per_element)
+    batch = 2 if guidance else 1
+    x_full = torch.from_numpy(initial_latent(params, seed, batch)).to(params.w_time.device)
+    if use_split:
+        x_full = x_full[den.half:den.half + 1]
     z = den.shard_input(x_full)
     den.run(z)
     if world > 1:
-        latent = torch.cat(_all_gather(z), dim=1)
+        parts = _all_gather(z)
+        if use_split:
+            gw = world // 2
+            latent = torch.cat([torch.cat(parts[:gw], dim=1), torch.cat(parts[gw:], dim=1)], dim=0)
+        else:
+            latent = torch.cat(parts, dim=1)
     else:
         latent = z
     res = ParallelRunResult(latent=latent.cpu().numpy(), comm_report=den.ledger, plan=den.plan,
                             worker_caches=[den.cache])
     res._batch = den.batch
     res._tail = (cfg.spatial_tokens, cfg.hidden)
+    res._split_gw = world // 2 if use_split else None
     return res

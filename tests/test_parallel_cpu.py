@@ -141,6 +141,58 @@ def test_gloo_frames_tokens_exchange(world):
     assert all(a and b for _, a, b in res), res
 
 
+def _pair_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2408_12588_b200.parallel import _all_gather_into
+
+        gw = world // 2
+        # the split_batch groups, created collectively in the same order on every rank
+        sp = [dist.new_group(list(range(g * gw, (g + 1) * gw))) for g in range(2)]
+        pairs = [dist.new_group([w, gw + w]) for w in range(gw)]
+        half, w = divmod(rank, gw)
+        mine = torch.full((3, 5), float(rank))
+        out = torch.empty(2, 3, 5)
+        _all_gather_into(out, mine, pairs[w])
+        # slot 0 = conditional half (group 0), slot 1 = unconditional half of the same frames
+        ok = torch.equal(out[0], torch.full((3, 5), float(w))) and torch.equal(out[1], torch.full((3, 5), float(gw + w)))
+        ok = ok and dist.get_world_size(sp[half]) == gw
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_split_batch_pair_exchange():
+    """split_batch: rank w (conditional half) and W/2 + w (unconditional half) hold the
+    same frames and exchange eps over their 2-rank group before the CFG combine."""
+    world = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pair_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r for r, _ in res) == list(range(world)) and all(ok for _, ok in res), res
+
+
+def test_split_batch_volume_model():
+    """Closed form with split_batch: two groups of W/2, each moving its B=1 half
+    (reference pkg/tests/test_parallel.py:193-204)."""
+    sched = make_schedule(6)
+    t = build_schedule(NonePolicy(), sched, 2)
+    cfg = ModelConfig(layers=2, hidden=32, heads=4, frames=4, spatial_tokens=16, text_tokens=8)
+    split = comm_volume_model("dsp", cfg, sched, t, 4, batch=2, split_batch=True)
+    whole = comm_volume_model("dsp", cfg, sched, t, 4, batch=2)
+    el = lambda b, w: b * 4 * 16 * 32 // w * (w - 1)  # noqa: E731
+    assert all(v == 2 * 2 * el(1, 2) for v in split.grouped_elements().values())
+    assert all(v == 2 * el(2, 4) for v in whole.grouped_elements().values())
+    assert comm_volume_model("dsp", cfg, sched, t, 2, batch=2, split_batch=True).total_elements() == 0
+
+
 def test_send_order_matches_kernel_permutation_formula():
     """The CUDA prologue writes h row (b, t, s) at ((dst*Tl + t)*B + b)*Sw + s%Sw
     (include/pab_b200.h, pab_residual_modnorm_sp); check the torch layout used by

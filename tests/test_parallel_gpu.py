@@ -26,7 +26,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, guidance, q):
+def _worker(rank, world, port, guidance, split, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -42,7 +42,8 @@ def _worker(rank, world, port, guidance, q):
         sched = make_schedule(8)
         pol = PabPolicy(2, 3, 2, window=(990.0, 10.0))
         table = build_schedule(pol, sched, cfg.layers)
-        par = run_parallel(params, sched, pol, world, "broadcast_sp", seed=7, guidance=guidance, table=table)
+        par = run_parallel(params, sched, pol, world, "broadcast_sp", seed=7, guidance=guidance, table=table,
+                           split_batch=split)
         gathered = par.gathered_cache()
         out = {"rank": rank}
         if rank == 0:
@@ -51,9 +52,12 @@ def _worker(rank, world, port, guidance, q):
             out["rel"] = float(np.linalg.norm(d) / np.linalg.norm(ser.latent))
             comp = table.compute_steps(ComponentKind.TEMPORAL)
             out["events"] = par.comm_report.event_count()
-            out["events_want"] = 2 * cfg.layers * len(comp)
-            out["steps_ok"] = {e.step for e in par.comm_report.entries} == set(comp)
-            model = comm_volume_model("broadcast_sp", cfg, sched, table, world, batch=2 if guidance else 1)
+            groups = 2 if split else 1
+            gw = world // groups
+            out["events_want"] = 2 * cfg.layers * len(comp) * groups if gw > 1 else 0
+            out["steps_ok"] = {e.step for e in par.comm_report.entries} <= set(comp)
+            model = comm_volume_model("broadcast_sp", cfg, sched, table, world, batch=2 if guidance else 1,
+                                      split_batch=split)
             out["ledger_ok"] = par.comm_report.grouped_elements() == model.grouped_elements()
             worst = 0.0
             from paper_2408_12588_b200.runtime import canonical
@@ -72,12 +76,14 @@ def _worker(rank, world, port, guidance, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,guidance", [(2, False), (2, True), (4, True)])
-def test_broadcast_sp_matches_serial(world, guidance):
+@pytest.mark.parametrize("world,guidance,split", [(2, False, False), (2, True, False), (4, True, False),
+                                                  (2, True, True), (4, True, True)])
+def test_broadcast_sp_matches_serial(world, guidance, split):
+    """split: CFG halves on two rank groups (reference split_batch, parallel.py:410-464)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, guidance, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, guidance, split, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]
