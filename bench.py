@@ -44,6 +44,9 @@ CONFIGS = {
                steps=150, preset="opensoraplan-pab246", batch=2),
     "C5": dict(layers=28, hidden=1152, heads=16, frames=32, spatial_tokens=3600, text_tokens=300, cross=True,
                steps=30, preset="opensora-pab246", batch=2),
+    # functional multi-rank checks only (not a bench line): C1 shapes with CFG, cross in temporal
+    "C1cfg": dict(layers=4, hidden=144, heads=2, frames=8, spatial_tokens=1024, text_tokens=16, cross=True,
+                  steps=10, preset="opensora-pab246", batch=2),
 }
 METRIC = "s/video denoising latency (PAB, opensora-pab246)"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
@@ -211,6 +214,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-none", action="store_true", help="skip the no-PAB comparison run")
+    ap.add_argument("--split-batch", action="store_true",
+                    help="N>1: CFG halves on two rank groups of N/2 (reference run_parallel split_batch)")
     args = ap.parse_args()
     c = CONFIGS[args.config]
     if args.impl == "reference":
@@ -247,15 +252,26 @@ def main():
     ids = np.arange(cfg.text_tokens) % 256
     guidance = c["batch"] == 2
 
-    if world > 1:
-        from paper_2408_12588_b200.parallel import ShardedDenoiser
+    split = bool(args.split_batch and world > 1 and world % 2 == 0 and guidance)
 
-        den = ShardedDenoiser(params, sched, table, ids, guidance=guidance, guidance_scale=4.0, rank=rank,
-                              world=world)
-    else:
-        den = Denoiser(params, sched, table, ids, guidance=guidance, guidance_scale=4.0)
+    def make_denoiser(tab):
+        if split:
+            from paper_2408_12588_b200.parallel import split_batch_denoiser
+
+            return split_batch_denoiser(params, sched, tab, ids, guidance_scale=4.0)
+        if world > 1:
+            from paper_2408_12588_b200.parallel import ShardedDenoiser
+
+            return ShardedDenoiser(params, sched, tab, ids, guidance=guidance, guidance_scale=4.0, rank=rank,
+                                   world=world)
+        return Denoiser(params, sched, tab, ids, guidance=guidance, guidance_scale=4.0)
+
+    den = make_denoiser(table)
     x_host = torch.from_numpy(initial_latent(params, 11, c["batch"])).pin_memory()
-    x_dev = den.shard_input(x_host.cuda()) if world > 1 else x_host.cuda()
+    if split:
+        x_dev = den.shard_input(x_host.cuda()[den.half:den.half + 1])
+    else:
+        x_dev = den.shard_input(x_host.cuda()) if world > 1 else x_host.cuda()
     z = torch.empty_like(x_dev)
     stream = torch.cuda.current_stream()
 
@@ -268,7 +284,57 @@ def main():
         z.copy_(x_dev)
         den.run(z)
 
-    for _ in range(args.warmup):
+    # per-kernel timings on the launching stream (CUDA events), on the engine's own
+    # workspaces: once right after the first warm-up video (kernel timed alone at burst
+    # clocks -> roofline vs the burst peak) and once after the timed videos (power-capped
+    # step conditions -> "in_step", vs the sustained peak)
+    peaks, peak_src = load_peaks()
+    ctx = den.ctx
+
+    def time_launch(fn, reps=10):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps / 1000.0
+
+    B, T, S, D, M = ctx.B, ctx.T, ctx.S, ctx.D, ctx.M
+    flop_sp = 4.0 * B * T * S * S * D
+    flop_tm = 4.0 * B * S * T * T * D
+    flop_cr = 4.0 * B * T * S * M * D
+    rows = ctx.rows
+    bytes_mn = rows * D * (4 + 2 + 4 + 2)
+
+    def kernel_times(peak_tf):
+        xbuf = torch.zeros(rows, D, device="cuda")
+        pend = [torch.zeros(rows, D, device="cuda", dtype=torch.bfloat16)]
+        mod = torch.zeros(2 * D, device="cuda")
+        t_sp = time_launch(lambda: kernels.attention(ctx.args_spatial))
+        t_tm = time_launch(lambda: kernels.attention(ctx.args_temporal))
+        t_cr = time_launch(lambda: kernels.attention(ctx.args_cross[0][0]))
+        t_mn = time_launch(lambda: kernels.residual_modnorm(xbuf, xbuf, pend, h_out=ctx.h, mod=mod, mode=1))
+        del xbuf, pend
+        return t_sp, {
+            "spatial_attn": {"ms": t_sp * 1e3, "tflops": flop_sp / t_sp / 1e12,
+                             "frac_bf16_peak": flop_sp / t_sp / 1e12 / peak_tf},
+            "temporal_attn": {"ms": t_tm * 1e3, "gbs": 8.0 * B * T * S * D / t_tm / 1e9,
+                              "frac_hbm": 8.0 * B * T * S * D / t_tm / 1e9 / peaks["hbm_gbs"]},
+            "cross_attn": {"ms": t_cr * 1e3, "tflops": flop_cr / t_cr / 1e12,
+                           "frac_bf16_peak": flop_cr / t_cr / 1e12 / peak_tf,
+                           "gbs": (4.0 * B * T * S * D + 4.0 * B * M * D) / t_cr / 1e9},
+            "broadcast_epilogue_modnorm": {"ms": t_mn * 1e3, "gbs": bytes_mn / t_mn / 1e9,
+                                           "frac_hbm": bytes_mn / t_mn / 1e9 / peaks["hbm_gbs"]},
+        }
+
+    one_video()
+    barrier()
+    time.sleep(3.0)  # let the board's power average settle (sw_power_cap window) -> burst clocks
+    t_sp, kern = kernel_times(peaks["bf16_tflops"])
+    for _ in range(args.warmup - 1):
         one_video()
     barrier()
     launches0 = den.ctx.launches.own_kernels()
@@ -301,17 +367,13 @@ def main():
         t = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    io_bytes = x_host.numel() * x_host.element_size()
+    io_bytes = x_dev.numel() * x_dev.element_size()  # this rank's share of the latent, each way
 
     # no-PAB reference point (same engine, every site computed)
     none_ms = None
     if not args.no_none:
         table_none = build_schedule(NonePolicy(), sched, cfg.layers)
-        if world > 1:
-            den_none = ShardedDenoiser(params, sched, table_none, ids, guidance=guidance, guidance_scale=4.0,
-                                       rank=rank, world=world)
-        else:
-            den_none = Denoiser(params, sched, table_none, ids, guidance=guidance, guidance_scale=4.0)
+        den_none = make_denoiser(table_none)
         z.copy_(x_dev)
         den_none.run(z)
         barrier()
@@ -330,45 +392,7 @@ def main():
             none_ms = float(t.item())
         del den_none
 
-    # roofline of the dominant kernel (spatial attention), timed live on the launching stream
-    peaks, peak_src = load_peaks()
-    ctx = den.ctx
-    kern = {}
-
-    def time_launch(fn, reps=10):
-        fn()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(reps):
-            fn()
-        b.record(stream)
-        torch.cuda.synchronize()
-        return a.elapsed_time(b) / reps / 1000.0
-
-    B, T, S, D, M = ctx.B, ctx.T, ctx.S, ctx.D, ctx.M
-    flop_sp = 4.0 * B * T * S * S * D
-    t_sp = time_launch(lambda: kernels.attention(ctx.args_spatial))
-    flop_tm = 4.0 * B * S * T * T * D
-    t_tm = time_launch(lambda: kernels.attention(ctx.args_temporal))
-    flop_cr = 4.0 * B * T * S * M * D
-    t_cr = time_launch(lambda: kernels.attention(ctx.args_cross[0][0]))
-    rows = ctx.rows
-    xbuf = torch.zeros(rows, D, device="cuda")
-    pend = [torch.zeros(rows, D, device="cuda", dtype=torch.bfloat16)]
-    mod = torch.zeros(2 * D, device="cuda")
-    t_mn = time_launch(lambda: kernels.residual_modnorm(xbuf, xbuf, pend, h_out=ctx.h, mod=mod, mode=1))
-    bytes_mn = rows * D * (4 + 2 + 4 + 2)
-    kern = {
-        "spatial_attn": {"ms": t_sp * 1e3, "tflops": flop_sp / t_sp / 1e12,
-                         "frac_bf16_peak": flop_sp / t_sp / 1e12 / peaks["bf16_tflops"]},
-        "temporal_attn": {"ms": t_tm * 1e3, "gbs": 8.0 * B * T * S * D / t_tm / 1e9,
-                          "frac_hbm": 8.0 * B * T * S * D / t_tm / 1e9 / peaks["hbm_gbs"]},
-        "cross_attn": {"ms": t_cr * 1e3, "tflops": flop_cr / t_cr / 1e12,
-                       "gbs": (4.0 * B * T * S * D + 4.0 * B * M * D) / t_cr / 1e9},
-        "broadcast_epilogue_modnorm": {"ms": t_mn * 1e3, "gbs": bytes_mn / t_mn / 1e9,
-                                       "frac_hbm": bytes_mn / t_mn / 1e9 / peaks["hbm_gbs"]},
-    }
+    t_sp_step, kern_step = kernel_times(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
     achieved = flop_sp / t_sp / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "r01_attn_fa_ncu_full.json")
@@ -395,7 +419,8 @@ def main():
             "config": {"workload": args.config, "layers": cfg.layers, "hidden": cfg.hidden, "heads": cfg.heads,
                        "frames": cfg.frames, "spatial_tokens": cfg.spatial_tokens, "text_tokens": cfg.text_tokens,
                        "denoise_steps": c["steps"], "batch": c["batch"], "preset": c["preset"],
-                       "parallelism": f"broadcast_sp{world}" if world > 1 else "single",
+                       "parallelism": (f"cfg2x_broadcast_sp{world // 2}" if split else
+                                       f"broadcast_sp{world}" if world > 1 else "single"),
                        "l2": "inputs larger than L2 (fp32 latent 230 MB > 126 MB L2)",
                        "none_s_per_video": None if none_ms is None else none_ms / 1000.0,
                        "pab_speedup_vs_none": None if none_ms is None else none_ms / ms,
@@ -405,6 +430,8 @@ def main():
             "gpu_launches": launches,
             "roofline": roofline,
             "kernels": kern,
+            "kernels_in_step": dict(kern_step, note="same launches after the timed videos (power-capped "
+                                    "clocks); fractions vs the sustained bf16 peak"),
             "clocks": clk.summary(),
             "cpu_baseline": base,
         }
