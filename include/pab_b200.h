@@ -102,6 +102,17 @@ int pab_ddim_cfg(float* z, const float* r, const void* const* pending, int n_pen
                  int batch, int64_t n_per_batch, int guidance, double guidance_scale,
                  double a_cur, double a_next, void* stream);
 
+/*
+ * Materialised attention probabilities for score broadcast (K10,
+ * broadcast_object="scores"). Replaces: numerics.softmax_rows after the
+ * logits *= 1/sqrt(dh) of scaled_dot_attention (pkg/src/pab_engine/numerics.py:
+ * 107-112, 133-151) as captured by model._attention_core (model.py:325-335).
+ *   p[r, j] = bf16( exp(scale*l[r, j] - m_r) / sum_j exp(scale*l[r, j] - m_r) ),
+ *   m_r = max_j scale*l[r, j]; l fp32 rows of length n (row stride ld_l), p bf16 (ld_p).
+ */
+int pab_softmax_rows(const float* logits, int64_t ld_l, void* p_bf16, int64_t ld_p, int64_t rows, int64_t n,
+                     float scale, void* stream);
+
 /* tanh-approximation GELU on bf16 (numerics.py:154-158), in may equal out. */
 int pab_gelu_bf16(const void* in, void* out, int64_t n, void* stream);
 

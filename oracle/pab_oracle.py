@@ -12,7 +12,8 @@ reference, all below the bf16 tolerance the GPU path is held to:
     single-accumulator loop (numerics.py:64-104) -> fp32 rounding order
     differs (~1e-6 relative); pinned against reference-generated fixtures in
     tests/golden/ (see tests/golden/make_golden.py and tests/test_oracle.py);
-  * broadcast_object="scores" (score replay) is not restated.
+  * broadcast_object="scores" (score replay, model.py:325-392, 476-493) keeps
+    the probabilities in float32 like the reference.
 Decision tables are integer work and are restated exactly.
 """
 
@@ -172,6 +173,37 @@ def site_output(cfg: Cfg, w: dict, li: int, kind: str, block: str, x, tvec, text
     return o @ w[p + ".o"]
 
 
+def _probs(q, k):
+    s = np.matmul(q, np.swapaxes(k, -1, -2)) * np.float32(1.0 / math.sqrt(q.shape[-1]))
+    return _softmax(s)
+
+
+def site_scores(cfg: Cfg, w: dict, li: int, kind: str, block: str, x, tvec, text, probs=None):
+    """Score broadcast (model.py:325-392): probs=None -> (o, P) computed with
+    capture; probs given -> o replayed as P @ v of the current input."""
+    d = cfg.D
+    if kind == "cross":
+        p = f"{li}.{'cs' if block == 's' else 'ct'}"
+        b, t, s, _ = x.shape
+        v = _heads(text @ w[p + ".v"], cfg.H)
+        if probs is None:
+            q = _heads((x @ w[p + ".q"]).reshape(b, t * s, d), cfg.H)
+            probs = _probs(q, _heads(text @ w[p + ".k"], cfg.H))
+            o = _unheads(np.matmul(probs, v)).reshape(b, t, s, d) @ w[p + ".o"]
+            return o, probs
+        return _unheads(np.matmul(probs, v)).reshape(b, t, s, d) @ w[p + ".o"]
+    p = f"{li}.{'sa' if kind == 'spatial' else 'ta'}"
+    mod = tvec @ w[p + ".mod"]
+    h = _ln(x) * (1.0 + mod[d:]) + mod[:d]
+    tr = (lambda a: a.transpose(0, 2, 1, 3)) if kind == "temporal" else (lambda a: a)
+    v = _heads(tr(h @ w[p + ".v"]), cfg.H)
+    ret = probs is None
+    if ret:
+        probs = _probs(_heads(tr(h @ w[p + ".q"]), cfg.H), _heads(tr(h @ w[p + ".k"]), cfg.H))
+    o = tr(_unheads(np.matmul(probs, v))) @ w[p + ".o"]
+    return (o, probs) if ret else o
+
+
 KIND_ORDER = ("spatial", "temporal", "cross", "mlp")  # table axis order (model.py:56-64)
 
 
@@ -203,8 +235,9 @@ def stores_of(table: np.ndarray) -> set:
     return out
 
 
-def forward(cfg, w, x, t, text, table, step, cache, log=None, delta_mode=False):
-    """One step (model.py:425-568); cache maps site -> (source step, value)."""
+def forward(cfg, w, x, t, text, table, step, cache, log=None, delta_mode=False, scores=False):
+    """One step (model.py:425-568); cache maps site -> (source step, value).
+    scores: broadcast_object="scores" (attention sites cache probabilities)."""
     tvec = time_embedding(t, cfg.D).astype(np.float32) @ w["time"]
     stores = stores_of(table) if not delta_mode else None
     for li in range(cfg.L):
@@ -219,14 +252,21 @@ def forward(cfg, w, x, t, text, table, step, cache, log=None, delta_mode=False):
             ki = KIND_ORDER.index(kind)
             src = int(row[ki])
             key = (li, kind, block)
+            score_site = scores and kind != "mlp"
             if src == step:
-                o = site_output(cfg, w, li, kind, block, x, tvec, text)
-                if not delta_mode and (step, li, ki) in stores:
-                    cache[key] = (step, o)
+                stored = not delta_mode and (step, li, ki) in stores
+                if score_site and stored:
+                    o, probs = site_scores(cfg, w, li, kind, block, x, tvec, text)
+                    cache[key] = (step, probs)
+                else:
+                    o = site_output(cfg, w, li, kind, block, x, tvec, text)
+                    if stored:
+                        cache[key] = (step, o)
                 dec = "compute"
             else:
-                cached_src, o = cache[key]
+                cached_src, val = cache[key]
                 assert cached_src == src, (key, cached_src, src)
+                o = site_scores(cfg, w, li, kind, block, x, tvec, text, probs=val) if score_site else val
                 dec = "reuse"
             if log is not None:
                 log.append((step, li, kind, block, dec, src))
@@ -250,7 +290,7 @@ def latent0(cfg: Cfg, seed: int, batch: int):
 
 
 def sample(cfg, w, timesteps, table, seed, text_ids=None, guidance=False, g=4.0, delta_mode=False,
-           per_step=None, log=None):
+           per_step=None, log=None, scores=False):
     """DDIM eta=0 sampler with optional CFG pair (diffusion.py:125-189)."""
     ab = alpha_bar_fn()
     batch = 2 if guidance else 1
@@ -261,7 +301,7 @@ def sample(cfg, w, timesteps, table, seed, text_ids=None, guidance=False, g=4.0,
     cache: dict = {}
     n = len(timesteps)
     for i, t in enumerate(timesteps):
-        eps = forward(cfg, w, x, t, text, table, i, cache, log=log, delta_mode=delta_mode)
+        eps = forward(cfg, w, x, t, text, table, i, cache, log=log, delta_mode=delta_mode, scores=scores)
         if guidance:
             eps = eps[1:2] + np.float32(g) * (eps[0:1] - eps[1:2])
         a, an = ab(t), (ab(timesteps[i + 1]) if i + 1 < n else 1.0)

@@ -432,6 +432,42 @@ extern "C" int pab_ddim_cfg(float* z, const float* r, const void* const* pending
     return launch_status("ddim_cfg");
 }
 
+// --------------------------------------------------------------------------
+// K10: row softmax of fp32 logits -> bf16 probabilities (score broadcast capture).
+// One warp per row, three passes over the row (L2-resident for rows <= 3600):
+// max of the scaled logits, sum of exp, normalised store.  expf / division in
+// fp32 as numpy's softmax_rows (numerics.py:107-112).
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) softmax_rows_kernel(const float* __restrict__ l, int64_t ld_l,
+                                                           __nv_bfloat16* __restrict__ p, int64_t ld_p,
+                                                           int64_t rows, int64_t n, float scale) {
+    const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const float* x = l + row * ld_l;
+    float m = -INFINITY;
+    for (int64_t j = lane; j < n; j += 32) m = fmaxf(m, x[j] * scale);
+    m = warp_max(m);
+    float sum = 0.f;
+    for (int64_t j = lane; j < n; j += 32) sum += expf(x[j] * scale - m);
+    sum = warp_sum(sum);
+    const float inv = 1.0f / sum;
+    __nv_bfloat16* y = p + row * ld_p;
+    for (int64_t j = lane; j < n; j += 32) y[j] = __float2bfloat16_rn(expf(x[j] * scale - m) * inv);
+}
+
+extern "C" int pab_softmax_rows(const float* logits, int64_t ld_l, void* p_bf16, int64_t ld_p, int64_t rows,
+                                int64_t n, float scale, void* stream) {
+    if (rows < 0 || n < 0 || ld_l < n || ld_p < n) return PAB_ERR_SHAPE;
+    if (rows == 0 || n == 0) return PAB_OK;
+    if (!logits || !p_bf16) return PAB_ERR_INVALID;
+    const int64_t blocks = (rows + 7) / 8;
+    if (blocks > 0x7fffffff) return PAB_ERR_UNSUPPORTED;
+    softmax_rows_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        logits, ld_l, reinterpret_cast<__nv_bfloat16*>(p_bf16), ld_p, rows, n, scale);
+    return launch_status("softmax_rows");
+}
+
 extern "C" int pab_gelu_bf16(const void* in, void* out, int64_t n, void* stream) {
     if (n < 0) return PAB_ERR_SHAPE;
     if (n == 0) return PAB_OK;

@@ -138,6 +138,20 @@ def ddim_cfg(z, r, pending, guidance: bool, guidance_scale: float, a_cur: float,
     )
 
 
+def softmax_rows(logits: torch.Tensor, p_out: torch.Tensor, scale: float) -> torch.Tensor:
+    """p_out (bf16) <- softmax(scale * logits) over the last axis (K10 score capture)."""
+    lib = _lib.load()
+    _need(logits, torch.float32, "logits")
+    _need(p_out, torch.bfloat16, "probabilities")
+    n = logits.shape[-1]
+    if p_out.shape != logits.shape or logits.stride(-1) != 1 or p_out.stride(-1) != 1:
+        raise ShapeError("softmax_rows needs equal shapes with unit column stride")
+    lv, pv = logits.reshape(-1, n), p_out.view(-1, n)
+    _lib.check(lib.pab_softmax_rows(lv.data_ptr(), lv.stride(0), pv.data_ptr(), pv.stride(0), lv.shape[0], n,
+                                    float(scale), _stream()), "pab_softmax_rows")
+    return p_out
+
+
 def gelu_(x: torch.Tensor) -> torch.Tensor:
     lib = _lib.load()
     _need(x, torch.bfloat16, "gelu input")

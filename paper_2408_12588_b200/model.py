@@ -419,10 +419,9 @@ def forward_step(
         raise ShapeError(f"latent shape {tuple(xt.shape)} does not match config {cfg}")
     if broadcast_object not in ("outputs", "scores"):
         raise ValidationError(f"unknown broadcast object {broadcast_object!r}")
-    if broadcast_object == "scores":
-        raise ValidationError("broadcast_object='scores' is not implemented on the B200 path (outputs only)")
     xt = xt.to(device=params.w_time.device, dtype=torch.float32).contiguous()
     ctx = StepContext.build(params, xt.shape[0], text_ids, [float(t)])
+    ctx.broadcast_object = broadcast_object
     r = torch.empty_like(xt)
     run_forward(ctx, 0, float(t), xt, r, decisions, cache, trace=trace, flop_sink=flop_sink, finish="residual")
     return r

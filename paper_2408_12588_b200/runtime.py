@@ -100,6 +100,7 @@ class StepContext:
         self.o_scratch_tm.pab_token_major = True
         self.shape3 = (batch, self.T, self.S)
         self.launches = Launches()
+        self.broadcast_object = "outputs"  # "scores": score broadcast (reference model.py:446-493)
         # debugging override (the default, "auto", selects the tcgen05 kernel for every model shape)
         self.attn_impl = {"auto": kernels.IMPL_AUTO, "tcgen05": kernels.IMPL_TCGEN05,
                           "simt": kernels.IMPL_SIMT}[os.environ.get("PAB_ATTN_IMPL", "auto")]
@@ -181,6 +182,26 @@ class _Sink:
         add(CAT_OUT, 2 * E * D)
 
 
+    def replay(self, kind):
+        """Score replay flops (reference model.py:336-392: modnorm + v projection for the
+        axis kinds, text v projection for cross, P.V, output projection)."""
+        if self.sink is None:
+            return
+        c = self.ctx
+        E = c.rows * c.D
+        D, H, dh = c.D, c.H, c.dh
+        add = lambda cat, n: self.sink.add(kind, cat, int(n))  # noqa: E731
+        if kind == CR:
+            add(CAT_QKV, 2 * (c.B * c.M) * D * D)
+            add(CAT_VALUE, 2 * c.B * H * c.T * c.S * dh * c.M)
+        else:
+            n = c.S if kind == SP else c.T
+            add(CAT_NORM_MOD, LN_FLOPS_PER_ELEM * E + 2 * D * 2 * D + MODULATE_FLOPS_PER_ELEM * E)
+            add(CAT_QKV, 2 * E * D)
+            add(CAT_VALUE, 2 * c.rows * H * dh * n)
+        add(CAT_OUT, 2 * E * D)
+
+
 class _Step:
     """Mutable state of one forward pass."""
 
@@ -231,28 +252,126 @@ class _Step:
             self.trace.observe(TraceRecord(step=self.step, timestep=self.t, layer=li, kind=kind, block=block,
                                            decision=decision, source_step=source), o)
 
-    def run_site(self, li, kind, block, compute, token_major=False):
+    def run_site(self, li, kind, block, compute, token_major=False, scores=None):
+        """scores: (capture, replay) closures of an attention site in score-broadcast
+        mode (reference model.py:469-499): a stored compute caches the bf16
+        probabilities instead of the output, a reuse replays them against the
+        current step's values."""
         d = self.decisions
         source = d.source(li, kind)
         site = (li, kind, block)
         c = self.ctx
         if source == self.step:
             store = d.should_store(li, kind)
-            o = compute(self.out_buffer(store, token_major))
-            if store:
-                self.cache.store(site, o, self.step, "outputs")
+            if scores is not None and store:
+                o, probs = scores[0](self.out_buffer(False, token_major))
+                self.cache.store(site, probs, self.step, "scores")
+            else:
+                o = compute(self.out_buffer(store, token_major))
+                if store:
+                    self.cache.store(site, o, self.step, "outputs")
             self.sink.site(kind, block)
             c.launches.sites_computed += 1
             decision = "compute"
         else:
-            entry = self.cache.fetch(site, "outputs")
+            entry = self.cache.fetch(site, "scores" if scores is not None else "outputs")
             if entry.source_step != source:
                 raise PolicyError(f"cache for {site} holds step {entry.source_step}, table expects {source}")
-            o = entry.value
+            if scores is not None:
+                o = scores[1](entry.value)
+                self.sink.replay(kind)
+            else:
+                o = entry.value
             c.launches.sites_reused += 1
             decision = "reuse"
         self.pending.append(o)
         self.record(li, kind, block, decision, source, o)
+
+    # -- score broadcast (K10) ---------------------------------------------
+    # Probabilities are materialised per (problem, head): logits by a cuBLAS
+    # batched GEMM with fp32 output, softmax by pab_softmax_rows into bf16 P,
+    # P.V by a cuBLAS batched GEMM.  Only taken when broadcast_object="scores"
+    # and the table stores the site; the paper measures this mode slower than
+    # output broadcast (PAPER Table 3), the default path never runs it.
+    def _split(self, x, problems, n):
+        c = self.ctx
+        return x.reshape(problems, n, c.H, c.dh).permute(0, 2, 1, 3).reshape(problems * c.H, n, c.dh)
+
+    def _merge_into_attn_out(self, out, problems, n):
+        c = self.ctx
+        c.attn_out.view(problems, n, c.H, c.dh).copy_(out.view(problems, c.H, n, c.dh).permute(0, 2, 1, 3))
+
+    def _qkv_heads(self, kind, blk):
+        c = self.ctx
+        D = c.D
+        if kind == CR:
+            kv = c.text_kv[self._li][blk]
+            return (self._split(c.qbuf, c.B, c.T * c.S), self._split(kv[:, :D], c.B, c.M),
+                    self._split(kv[:, D:], c.B, c.M), c.B, c.T * c.S)
+        problems, n = (c.B * c.T, c.S) if kind == SP else (c.B * c.S, c.T)  # temporal rows are token-major
+        q, k, v = (self._split(c.qkv[:, i * D:(i + 1) * D], problems, n) for i in range(3))
+        return q, k, v, problems, n
+
+    def _probs_out(self, kind, blk):
+        c = self.ctx
+        q, k, v, problems, n = self._qkv_heads(kind, blk)
+        logits = torch.bmm(q, k.transpose(1, 2), out_dtype=torch.float32)
+        probs = torch.empty(logits.shape, device=logits.device, dtype=torch.bfloat16)
+        kernels.softmax_rows(logits, probs, 1.0 / float(np.sqrt(c.dh)))
+        del logits
+        self._merge_into_attn_out(torch.bmm(probs, v), problems, n)
+        c.launches.other_calls += 1
+        c.launches.gemm_calls += 2
+        return probs
+
+    def attn_scores(self, p, slot, temporal):
+        c = self.ctx
+        kind = TM if temporal else SP
+
+        def capture(o):
+            self.prologue(1, self.mods[self._li, slot], (p.ln_gamma, p.ln_beta), token_major=temporal)
+            torch.mm(c.h, p.w_qkv, out=c.qkv)
+            probs = self._probs_out(kind, None)
+            torch.mm(c.attn_out, p.wo, out=o)
+            c.launches.gemm_calls += 2
+            return o, probs
+
+        def replay(probs):
+            # reference _axis_attention_replay (model.py:362-373): modnorm -> v only -> P.V -> wo
+            # v through the same fused QKV GEMM as the capture step, so replaying on an unchanged
+            # input reproduces the computed output bit for bit (reference test_model.py:138-151)
+            self.prologue(1, self.mods[self._li, slot], (p.ln_gamma, p.ln_beta), token_major=temporal)
+            torch.mm(c.h, p.w_qkv, out=c.qkv)
+            _, _, v, problems, n = self._qkv_heads(kind, None)
+            self._merge_into_attn_out(torch.bmm(probs, v), problems, n)
+            o = self.out_buffer(True, temporal)  # fresh: pending terms may still reference scratch
+            torch.mm(c.attn_out, p.wo, out=o)
+            c.launches.gemm_calls += 3
+            return o
+
+        return capture, replay
+
+    def cross_scores(self, p, blk):
+        c = self.ctx
+
+        def capture(o):
+            self.prologue(2)
+            torch.mm(c.h, p.wq, out=c.qbuf)
+            probs = self._probs_out(CR, blk)
+            torch.mm(c.attn_out, p.wo, out=o)
+            c.launches.gemm_calls += 2
+            return o, probs
+
+        def replay(probs):
+            # reference _cross_attention_replay (model.py:388-395): text v -> P.V -> wo; x untouched
+            kv = c.text_kv[self._li][blk]
+            self._merge_into_attn_out(torch.bmm(probs, self._split(kv[:, c.D:], c.B, c.M)), c.B, c.T * c.S)
+            o = self.out_buffer(True)
+            torch.mm(c.attn_out, p.wo, out=o)
+            c.launches.gemm_calls += 2
+            return o
+
+        return capture, replay
 
     # -- site bodies -------------------------------------------------------
     def attn_site(self, p, slot, temporal):
@@ -317,15 +436,20 @@ class _Step:
         if delta:
             self.flush()
             x_in = self.r.clone()
-        self.run_site(li, SP, "s", self.attn_site(lp.spatial, MOD_SPATIAL, False))
-        self.run_site(li, CR, "s", self.cross_site(lp.cross_spatial, 0))
+        sc = self.ctx.broadcast_object == "scores"
+        self.run_site(li, SP, "s", self.attn_site(lp.spatial, MOD_SPATIAL, False),
+                      scores=self.attn_scores(lp.spatial, MOD_SPATIAL, False) if sc else None)
+        self.run_site(li, CR, "s", self.cross_site(lp.cross_spatial, 0),
+                      scores=self.cross_scores(lp.cross_spatial, 0) if sc else None)
         self.run_site(li, ML, "s", self.mlp_site(lp.mlp_spatial, MOD_MLP_S))
         if temporal_hook is not None:
             temporal_hook(self, li, lp)
         else:
-            self.run_site(li, TM, "t", self.attn_site(lp.temporal, MOD_TEMPORAL, True), token_major=True)
+            self.run_site(li, TM, "t", self.attn_site(lp.temporal, MOD_TEMPORAL, True), token_major=True,
+                          scores=self.attn_scores(lp.temporal, MOD_TEMPORAL, True) if sc else None)
         if self.ctx.cfg.cross_in_temporal:
-            self.run_site(li, CR, "t", self.cross_site(lp.cross_temporal, 1))
+            self.run_site(li, CR, "t", self.cross_site(lp.cross_temporal, 1),
+                          scores=self.cross_scores(lp.cross_temporal, 1) if sc else None)
         self.run_site(li, ML, "t", self.mlp_site(lp.mlp_temporal, MOD_MLP_T))
         if x_in is not None and d.should_store_delta(li):
             self.flush()
@@ -334,7 +458,8 @@ class _Step:
 
 def run_forward(ctx: StepContext, step_index: int, t: float, z, r, decisions, cache, trace=None, flop_sink=None,
                 finish="residual", ddim=None, temporal_hook=None):
-    """Run every layer of one step.  finish="residual": r <- eps.
+    """Run every layer of one step (ctx.broadcast_object selects output or score
+    broadcast).  finish="residual": r <- eps.
     finish="ddim": z <- DDIM(z, CFG(eps)) with ddim=(guidance, g, a_cur, a_next)."""
     st = _Step(ctx, step_index, t, z, r, decisions, cache, trace, flop_sink)
     st.step = decisions.step

@@ -93,7 +93,7 @@ def prng():
     np.savez_compressed(os.path.join(OUT, "prng.npz"), **out)
 
 
-def _loop(params, sched, table, seed, guidance, ids=None):
+def _loop(params, sched, table, seed, guidance, ids=None, broadcast_object="outputs"):
     """Reference forward_step + ddim_update, recording every step's latent."""
     cfg = params.cfg
     ids = rd.default_text_ids(params) if ids is None else ids
@@ -105,7 +105,8 @@ def _loop(params, sched, table, seed, guidance, ids=None):
     steps = []
     ts = sched.timesteps
     for i, t in enumerate(ts):
-        eps = rm.forward_step(params, x, t, ids2, table.slice(i), cache, trace=trace)
+        eps = rm.forward_step(params, x, t, ids2, table.slice(i), cache, trace=trace,
+                              broadcast_object=broadcast_object)
         if guidance:
             eps = eps[1:2] + 4.0 * (eps[0:1] - eps[1:2])
         a = rd.DEFAULT_NOISE.alpha_bar(t)
@@ -153,6 +154,40 @@ def small_runs():
         json.dump(meta, fh, indent=0)
 
 
+def scores_runs():
+    """broadcast_object="scores" (attention sites cache probabilities, model.py:469-499)."""
+    out = {}
+    cases = {
+        "small": rm.ModelConfig(layers=2, hidden=32, heads=4, frames=4, spatial_tokens=16, text_tokens=8),
+        "smallx": rm.ModelConfig(layers=2, hidden=48, heads=2, frames=4, spatial_tokens=24, text_tokens=5,
+                                 cross_in_temporal=True),
+    }
+    policies = {
+        "pab": rp.PabPolicy(2, 4, 3, window=(990.0, 10.0),
+                            mlp=rp.MlpBroadcast(triggers=(700.0,), blocks=(0,), range=2)),
+        "tgate": rp.TGatePolicy(gate_step=4, interval=2, warmup=1),
+    }
+    meta = {}
+    for cname, cfg in cases.items():
+        params = rm.init_model(cfg, seed=3)
+        sched = rd.make_schedule(8)
+        for pname, pol in policies.items():
+            for guidance in (False, True):
+                table = rp.build_schedule(pol, sched, cfg.layers)
+                lat, log = _loop(params, sched, table, seed=7, guidance=guidance, broadcast_object="scores")
+                key = f"{cname}|{pname}|{int(guidance)}"
+                out[key + "|latents"] = lat.astype(np.float32)
+                out[key + "|log"] = log
+                out[key + "|table"] = table.source
+                meta[key] = {"policy": rp.policy_to_dict(pol)}
+        meta[cname] = {"layers": cfg.layers, "hidden": cfg.hidden, "heads": cfg.heads, "frames": cfg.frames,
+                       "spatial_tokens": cfg.spatial_tokens, "text_tokens": cfg.text_tokens,
+                       "cross_in_temporal": cfg.cross_in_temporal}
+    np.savez_compressed(os.path.join(OUT, "scores_runs.npz"), **out)
+    with open(os.path.join(OUT, "scores_runs.json"), "w") as fh:
+        json.dump(meta, fh, indent=0)
+
+
 def c1_run():
     cfg = rm.ModelConfig(layers=4, hidden=144, heads=2, frames=8, spatial_tokens=1024, text_tokens=16)
     params = rm.init_model(cfg, seed=11)
@@ -168,7 +203,7 @@ def c1_run():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["decisions", "prng", "small", "c1"]
+    which = sys.argv[1:] or ["decisions", "prng", "small", "c1", "scores"]
     if "decisions" in which:
         decisions()
     if "prng" in which:
@@ -177,4 +212,6 @@ if __name__ == "__main__":
         small_runs()
     if "c1" in which:
         c1_run()
+    if "scores" in which:
+        scores_runs()
     print("golden fixtures written to", OUT)

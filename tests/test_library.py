@@ -17,7 +17,8 @@ def declared_symbols():
 
 def test_header_declares_entry_points():
     syms = declared_symbols()
-    for need in ("pab_attention", "pab_residual_modnorm", "pab_ddim_cfg", "pab_gelu_bf16", "pab_fill_uniform"):
+    for need in ("pab_attention", "pab_residual_modnorm", "pab_ddim_cfg", "pab_gelu_bf16", "pab_fill_uniform",
+                 "pab_softmax_rows"):
         assert need in syms
 
 
@@ -41,6 +42,8 @@ def test_argument_validation_without_gpu():
     lib = _lib.load()
     # negative sizes are rejected on the host before any launch
     assert lib.pab_gelu_bf16(None, None, -1, None) == 1
+    assert lib.pab_softmax_rows(None, 4, None, 4, -1, 4, 1.0, None) == 1
+    assert lib.pab_softmax_rows(None, 4, None, 4, 0, 4, 1.0, None) == 0
     assert lib.pab_ddim_cfg(None, None, None, 0, 3, 10, 1, 4.0, 0.5, 0.6, None) == 1  # guidance needs batch 2
     args = _lib.AttnArgs()
     assert lib.pab_attention(ctypes.byref(args), 0, None) == 1  # null pointers

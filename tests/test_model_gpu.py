@@ -51,9 +51,10 @@ def assert_latent_close(got, want, tag, guided=False):
     return rel
 
 
-def run_steps(params, sched, table, seed, guidance, ids=None):
+def run_steps(params, sched, table, seed, guidance, ids=None, broadcast_object="outputs"):
     ids = np.arange(params.cfg.text_tokens) % 256 if ids is None else ids
-    den = Denoiser(params, sched, table, ids, guidance=guidance, guidance_scale=4.0)
+    den = Denoiser(params, sched, table, ids, guidance=guidance, guidance_scale=4.0,
+                   broadcast_object=broadcast_object)
     z = torch.from_numpy(initial_latent(params, seed, den.batch)).cuda()
     steps = []
     den.run(z, on_step=lambda i, zz: steps.append(zz.cpu().numpy().copy()))
@@ -102,6 +103,72 @@ def test_small_runs_match_reference(small, case, policy, guidance):
     for i, (got, want) in enumerate(zip(steps, data[key + "|latents"])):
         assert_latent_close(got, want, (key, i), guided=bool(guidance))
     assert np.array_equal(log_array(den), data[key + "|log"])
+
+
+@pytest.fixture(scope="module")
+def scores_runs(golden_dir):
+    return (np.load(os.path.join(golden_dir, "scores_runs.npz")),
+            json.load(open(os.path.join(golden_dir, "scores_runs.json"))))
+
+
+@pytest.mark.parametrize("case", ["small", "smallx"])
+@pytest.mark.parametrize("policy", ["pab", "tgate"])
+@pytest.mark.parametrize("guidance", [0, 1])
+def test_scores_mode_matches_reference(scores_runs, case, policy, guidance):
+    """broadcast_object="scores" on the device (K10 capture + P.V replay) vs the
+    reference's own score-broadcast runs: decision log bit-exact, latents within
+    the bf16 tolerance; replay sites launch no QK^T or softmax."""
+    data, meta = scores_runs
+    m = meta[case]
+    key = f"{case}|{policy}|{guidance}"
+    cfg = ModelConfig(layers=m["layers"], hidden=m["hidden"], heads=m["heads"], frames=m["frames"],
+                      spatial_tokens=m["spatial_tokens"], text_tokens=m["text_tokens"],
+                      cross_in_temporal=m["cross_in_temporal"])
+    params = init_model(cfg, seed=3)
+    table = DecisionTable(data[key + "|table"])
+    steps, den = run_steps(params, make_schedule(8), table, seed=7, guidance=bool(guidance),
+                           broadcast_object="scores")
+    for i, (got, want) in enumerate(zip(steps, data[key + "|latents"])):
+        assert_latent_close(got, want, (key, i), guided=bool(guidance))
+    assert np.array_equal(log_array(den), data[key + "|log"])
+    kinds = {e.object_kind for e in den.cache.entries.values()}
+    assert "scores" in kinds
+
+
+def test_scores_replay_identity_and_kind_checks():
+    """reference test_model.py:138-151, 177-186: on an unchanged input the score
+    replay reproduces the computed eps (bitwise: same GEMMs, same P); replaying
+    scores from an outputs cache is a PolicyError."""
+    cfg = ModelConfig(layers=2, hidden=144, heads=2, frames=4, spatial_tokens=64, text_tokens=6,
+                      cross_in_temporal=True)
+    params = init_model(cfg, seed=3)
+    x = initial_latent(params, seed=2, batch=1)
+    src = np.zeros((2, cfg.layers, 4), dtype=np.int32)
+    table = DecisionTable(src)
+    ids = np.arange(cfg.text_tokens)
+    res = {}
+    for mode in ("outputs", "scores"):
+        cache = CacheStore()
+        a = forward_step(params, x, 500.0, ids, table.slice(0), cache, broadcast_object=mode).cpu().numpy()
+        b = forward_step(params, x, 500.0, ids, table.slice(1), cache, broadcast_object=mode).cpu().numpy()
+        assert np.array_equal(a, b), mode
+        res[mode] = b
+    assert_latent_close(res["scores"], res["outputs"], "scores vs outputs replay")
+    cache = CacheStore()
+    forward_step(params, x, 500.0, ids, table.slice(0), cache, broadcast_object="outputs")
+    with pytest.raises(PolicyError):
+        forward_step(params, x, 500.0, ids, table.slice(1), cache, broadcast_object="scores")
+
+
+def test_softmax_rows_kernel():
+    torch.manual_seed(0)
+    for n in (1, 5, 300, 1560):
+        lg = torch.randn(37, n, device="cuda") * 4
+        p = torch.empty(37, n, device="cuda", dtype=torch.bfloat16)
+        kernels.softmax_rows(lg, p, 0.3)
+        want = torch.softmax(lg * 0.3, dim=-1)
+        assert (p.float() - want).abs().max().item() <= 4e-3 * max(want.max().item(), 1e-3), n
+        assert torch.allclose(p.float().sum(-1), torch.ones(37, device="cuda"), atol=n * 4e-3)
 
 
 def test_c1_latte_pab235_matches_reference(golden_dir):

@@ -82,3 +82,28 @@ def test_oracle_c1_subsample(golden_dir):
         rel = np.linalg.norm(sub - g["sub"][i]) / np.linalg.norm(g["sub"][i])
         assert rel < 1e-4, (i, rel)
         assert abs(np.linalg.norm(flat.astype(np.float64)) / g["norms"][i] - 1.0) < 1e-5
+
+
+@pytest.fixture(scope="module")
+def scores_runs(golden_dir):
+    return (np.load(os.path.join(golden_dir, "scores_runs.npz")),
+            json.load(open(os.path.join(golden_dir, "scores_runs.json"))))
+
+
+@pytest.mark.parametrize("case", ["small", "smallx"])
+@pytest.mark.parametrize("policy", ["pab", "tgate"])
+@pytest.mark.parametrize("guidance", [0, 1])
+def test_oracle_scores_mode_matches_reference_runs(scores_runs, case, policy, guidance):
+    """broadcast_object="scores": attention sites cache probabilities and replay
+    them against the current values (reference model.py:325-392, 469-499)."""
+    data, meta = scores_runs
+    key = f"{case}|{policy}|{guidance}"
+    m = meta[case]
+    cfg = orc.Cfg(m["layers"], m["hidden"], m["heads"], m["frames"], m["spatial_tokens"], m["text_tokens"],
+                  cross_in_temporal=m["cross_in_temporal"])
+    steps = []
+    orc.sample(cfg, orc.init_weights(cfg, seed=3), orc.linear_timesteps(8), data[key + "|table"], seed=7,
+               guidance=bool(guidance), per_step=steps, scores=True)
+    for i, (got, want) in enumerate(zip(steps, data[key + "|latents"])):
+        rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+        assert rel < 2e-5, (key, i, rel)
