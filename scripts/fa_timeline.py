@@ -16,6 +16,11 @@ out = torch.empty(rows, D, device="cuda", dtype=torch.bfloat16)
 ld = 3 * D
 a = kernels.attn_args(qkv[:, :D], qkv[:, D:2 * D], qkv[:, 2 * D:], out, (S * ld, 0, ld), (S * ld, 0, ld),
                       (S * ld, 0, ld), (S * D, 0, D), B * T, 1, S, S, H, dh)
+if len(sys.argv) > 1 and sys.argv[1] == "cross":  # C3 cross site: 300 text keys per batch entry
+    M = 300
+    kv = torch.randn(B * M, 2 * D, device="cuda").to(torch.bfloat16)
+    a = kernels.attn_args(qkv[:, :D], kv[:, :D], kv[:, D:], out, (T * S * ld, 0, ld), (M * 2 * D, 0, 2 * D),
+                          (M * 2 * D, 0, 2 * D), (T * S * D, 0, D), B, 1, T * S, M, H, dh)
 buf = torch.zeros(64 * 2 * 16, dtype=torch.int64, device="cuda")
 lib = _lib.load()
 for _ in range(3):
