@@ -54,6 +54,10 @@ constexpr int kFixWarp = kSoftmaxWarps + 2;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kSCol = 0, kPCol = 384;
 
+#ifndef PAB_FA_BULK_EPI
+#define PAB_FA_BULK_EPI 1   // O rows leave through smem staging + cp.async.bulk (0: direct stores)
+#endif
+
 #ifndef PAB_FA_POLY_DIV
 #define PAB_FA_POLY_DIV 3   // one column pair in PAB_FA_POLY_DIV on the FMA pipe (0: MUFU only)
 #endif
@@ -89,15 +93,22 @@ template <int N128, int N32, int NV>
 struct Geometry {
     static constexpr int kDhK = 64 * N128 + 16 * N32;
     static constexpr int kOCols = 16 * NV;
-    static constexpr int kSlot = 20480;  // one 128-row operand slot (Q, K or V), any dh <= 80
+    static constexpr int kSlot = 20480;    // one 128-row Q slot, any dh <= 80
+    // 112-row K/V slots: K = SW128 block (112 x 128 B) then SW32 blocks (112 x 32 B each);
+    // V = NV SW32 atoms of 16 columns, 112 x 32 B each
+    static constexpr int kK128 = kKv * 128, kK32 = kKv * 32, kVAtom = kKv * 32;
+    static constexpr int kSlotKV = 18432;
     static constexpr int kQ0 = 0;        // 2 item buffers x 2 tiles
-    static constexpr int kK0 = 4 * kSlot;  // 3-stage K ring
-    static constexpr int kV0 = 7 * kSlot;  // 3-stage V ring
-    static constexpr int kX0 = 10 * kSlot;                 // row-max exchange [2][2][2][128] f32
-    static constexpr int kBar = kX0 + 8 * kRows * 4;
+    static constexpr int kK0 = 4 * kSlot;                  // 3-stage K ring
+    static constexpr int kV0 = kK0 + 3 * kSlotKV;          // 3-stage V ring
+    static constexpr int kX0 = kV0 + 3 * kSlotKV;          // row-max exchange [2][2][2][128] f32 (split 2)
+    static constexpr int kStageRow = 144;                  // epilogue staging: max bytes of one bf16 O row
+    static constexpr int kX0Bytes = (2 * kRows * kStageRow > 8 * kRows * 4) ? 2 * kRows * kStageRow : 8 * kRows * 4;
+    static constexpr int kBar = kX0 + kX0Bytes;
     static constexpr int kSmem = kBar + 512 + 1024;  // + barriers + alignment slack
     static constexpr uint32_t kOCol0 = 224, kOStride = kOCols;
-    static_assert(N128 * 16384 + N32 * 4096 <= kSlot && NV * 4096 <= kSlot, "operand slot");
+    static_assert(N128 * 16384 + N32 * 4096 <= kSlot, "Q slot");
+    static_assert(N128 * kK128 + N32 * kK32 <= kSlotKV && NV * kVAtom <= kSlotKV && kSlotKV % 1024 == 0, "K/V slot");
     static_assert(kOCol0 + 2 * kOCols <= kPCol, "O tiles overlap P in TMEM");
     static_assert(kSmem <= 232448, "attention tiles exceed the 227 KB shared memory of one CTA");
 };
@@ -286,7 +297,8 @@ template <int N128, int N32, int NV>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fa_kernel(const __grid_constant__ CUtensorMap q128, const __grid_constant__ CUtensorMap q32,
                    const __grid_constant__ CUtensorMap k128, const __grid_constant__ CUtensorMap k32,
-                   const __grid_constant__ CUtensorMap v32, const Params p) {
+                   const __grid_constant__ CUtensorMap v32, const __grid_constant__ CUtensorMap omap,
+                   const Params p) {
     using G = Geometry<N128, N32, NV>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -318,6 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     // ---------------------------------------------------------------- setup
     if (warp == kTmaWarp && lane == 0) {
+        prefetch_map(&omap);
         prefetch_map(&q128);
         prefetch_map(&k128);
         prefetch_map(&v32);
@@ -387,6 +400,45 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool store = i < p.n_q;
             __nv_bfloat16* dst = p.o + (int64_t)it.a_idx * p.o_sa + (int64_t)it.b_idx * p.o_sb + (int64_t)i * p.o_si +
                                  (int64_t)it.h * p.dh;
+            if (kSplit == 1 && PAB_FA_BULK_EPI) {
+                // Every CTA reaches its epilogue at about the same time, so plain row stores form a
+                // GPU-wide write burst the softmax warps stall on (measured: not writing O at all
+                // makes cross attention 14% faster).  Stage the tile's 128 rows in smem and let
+                // one thread hand them to the TMA engine as ONE asynchronous tensor store (rows
+                // past n_q are clipped by the tensor map); the warps go on at once.
+                uint8_t* stg_tile = smem + G::kX0 + t * kRows * G::kStageRow;
+                uint8_t* stg = stg_tile + row * (2 * p.dh);  // dense rows: the TMA box layout
+                const bool issuer = (wl == 0 && lane == 0);
+                if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // last store read stg
+                asm volatile("bar.sync %0, 128;" ::"r"(1 + t) : "memory");
+                for (int cc = 0; 16 * cc < p.dh; ++cc) {
+                    PAB_TMEM_LD16(o_tmem + 16 * cc, o);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 16; e += 8) {
+                        if (16 * cc + e < p.dh) {
+                            uint32_t w[4];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) w[q] = pack_bf16(o[e + 2 * q] * inv, o[e + 2 * q + 1] * inv);
+                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(stg + (16 * cc + e) * 2)),
+                                         "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                                         : "memory");
+                        }
+                    }
+                }
+                fence_async_smem();  // generic-proxy smem writes -> visible to the TMA (async proxy)
+                asm volatile("bar.sync %0, 128;" ::"r"(1 + t) : "memory");
+#ifndef PAB_FA_DIAG_EPI_NOSTORE
+                if (issuer)
+                    asm volatile(
+                        "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];\n\t"
+                        "cp.async.bulk.commit_group;" ::"l"(reinterpret_cast<uint64_t>(&omap)),
+                        "r"(smem_u32(stg_tile)), "r"(0), "r"(it.h), "r"((it.tile0 + t) * kRows), "r"(it.b_idx),
+                        "r"(it.a_idx)
+                        : "memory");
+#endif
+                return;
+            }
             for (int cc = oc_lo; cc < oc_hi; ++cc) {
                 if (16 * cc >= p.dh) break;
                 PAB_TMEM_LD16(o_tmem + 16 * cc, o);
@@ -551,6 +603,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             epilogue(prev);
         }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // tile stores complete before exit
     } else if (warp == kTmaWarp) {
         // ===================================================== TMA producer
         if (lane == 0) {
@@ -576,21 +629,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int j = 0; j < n_kv; ++j, ++g) {
                     const int st = g % 3;
                     if (g >= 3) mbar_wait(&bars->k_empty[st], ((g / 3) - 1) & 1);
-                    uint8_t* kd = smem + G::kK0 + st * G::kSlot;
+                    uint8_t* kd = smem + G::kK0 + st * G::kSlotKV;
                     mbar_expect_tx(&bars->k_full[st], kKBytes);
                     for (int blk = 0; blk < N128; ++blk)
-                        tma_load_5d(kd + blk * 16384, &k128, &bars->k_full[st], 64 * blk, it.h, j * kKv, it.b_idx,
+                        tma_load_5d(kd + blk * G::kK128, &k128, &bars->k_full[st], 64 * blk, it.h, j * kKv, it.b_idx,
                                     it.a_idx);
                     for (int blk = 0; blk < N32; ++blk)
-                        tma_load_5d(kd + N128 * 16384 + blk * 4096, &k32, &bars->k_full[st], 64 * N128 + 16 * blk,
+                        tma_load_5d(kd + N128 * G::kK128 + blk * G::kK32, &k32, &bars->k_full[st], 64 * N128 + 16 * blk,
                                     it.h, j * kKv, it.b_idx, it.a_idx);
                     // V as 16-column SW32 atoms ([atom][row][32 B], atoms 4 KB apart): one MN-major
                     // descriptor spans the padded head dim; atom NV-1 holds the row-sum column
                     if (g >= 3) mbar_wait(&bars->v_empty[st], ((g / 3) - 1) & 1);
-                    uint8_t* vd = smem + G::kV0 + st * G::kSlot;
+                    uint8_t* vd = smem + G::kV0 + st * G::kSlotKV;
                     mbar_expect_tx(&bars->v_full[st], kVBytes);
                     for (int blk = 0; blk < NV; ++blk)
-                        tma_load_5d(vd + blk * 4096, &v32, &bars->v_full[st], 16 * blk, it.h, j * kKv, it.b_idx,
+                        tma_load_5d(vd + blk * G::kVAtom, &v32, &bars->v_full[st], 16 * blk, it.h, j * kKv, it.b_idx,
                                     it.a_idx);
                 }
             }
@@ -600,11 +653,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the P.V MMA then accumulates the row sums into O[:, dh].
         // SW32 atom layout: row r at 32 r, 16-byte chunk index XOR (r >> 2) & 1.
         const int col = p.dh % 16;
-        const uint32_t atom_off = (uint32_t)(p.dh / 16) * 4096u;
+        const uint32_t atom_off = (uint32_t)(p.dh / 16) * (uint32_t)G::kVAtom;
         for (int g = 0; g < n_iters; ++g) {
             const int st = g % 3;
             mbar_wait(&bars->v_full[st], (g / 3) & 1);
-            uint8_t* vd = smem + G::kV0 + st * G::kSlot + atom_off;
+            uint8_t* vd = smem + G::kV0 + st * G::kSlotKV + atom_off;
             for (int r = lane; r < kKv; r += 32) {
                 const uint32_t chunk = (uint32_t)(col >> 3) ^ (uint32_t)((r >> 2) & 1);
                 *reinterpret_cast<__nv_bfloat16*>(vd + r * 32 + chunk * 16 + (col & 7) * 2) = __float2bfloat16_rn(1.0f);
@@ -624,8 +677,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr uint32_t kHi128 = (1024u >> 4) | (1u << 14) | (kLayoutSW128 << 29);
         constexpr uint32_t kHi32 = (256u >> 4) | (1u << 14) | (kLayoutSW32 << 29);
         constexpr uint32_t kLbo16 = (16u >> 4) << 16;
-        // V: MN-major SW32, 16-column atoms 4096 B apart (LBO), 8-row groups 256 B apart (SBO)
-        constexpr uint32_t kLboV = (4096u >> 4) << 16;
+        // V: MN-major SW32, 16-column atoms kVAtom B apart (LBO), 8-row groups 256 B apart (SBO)
+        constexpr uint32_t kLboV = ((uint32_t)G::kVAtom >> 4) << 16;
         auto cols_of = [&](int j) {
             const int n = min(kKv, p.n_k - j * kKv);
             return (n + 15) & ~15;
@@ -634,14 +687,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // two tiles interleaved: MMAs on one accumulator serialise at ~80 cycles each, two
         // independent accumulators keep the tensor pipe busy.  ncols = keys rounded up to 16.
         auto issue_s = [&](int qb, int kst, int ncols, bool two) {
-            const uint32_t ka = k_lo + ((kst * G::kSlot) >> 4);
+            const uint32_t ka = k_lo + ((kst * G::kSlotKV) >> 4);
             const uint32_t qa0 = q_lo + ((2 * qb * G::kSlot) >> 4);
             const uint32_t idS = (idS128 & ~(0x3Fu << 17)) | ((uint32_t)(ncols >> 3) << 17);
             if (N128 == 1 && N32 == 1) {
                 const uint64_t dq = ((uint64_t)kHi128 << 32) | (qa0 | kLbo16);
                 const uint64_t dk = ((uint64_t)kHi128 << 32) | (ka | kLbo16);
                 const uint64_t dq32 = ((uint64_t)kHi32 << 32) | ((qa0 + (16384 >> 4)) | kLbo16);
-                const uint64_t dk32 = ((uint64_t)kHi32 << 32) | ((ka + (16384 >> 4)) | kLbo16);
+                const uint64_t dk32 = ((uint64_t)kHi32 << 32) | ((ka + (G::kK128 >> 4)) | kLbo16);
                 mma_group_s_72(tmem + kSCol, tmem + kSCol + kKv, dq, dk, dq32, dk32, idS, two, G::kSlot >> 4);
                 return;
             }
@@ -651,18 +704,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t d_s = tmem + kSCol + kKv * t;
                 for (int blk = 0; blk < N128; ++blk)
                     for (int k = 0; k < 4; ++k) {
-                        const uint32_t o = (blk * 16384 + 32 * k) >> 4;
-                        mma_ss1(d_s, (qa + o) | kLbo16, kHi128, (ka + o) | kLbo16, kHi128, idS, (blk | k) != 0);
+                        const uint32_t oq = (blk * 16384 + 32 * k) >> 4, ok = (blk * G::kK128 + 32 * k) >> 4;
+                        mma_ss1(d_s, (qa + oq) | kLbo16, kHi128, (ka + ok) | kLbo16, kHi128, idS, (blk | k) != 0);
                     }
                 for (int blk = 0; blk < N32; ++blk) {
-                    const uint32_t o = (N128 * 16384 + blk * 4096) >> 4;
-                    mma_ss1(d_s, (qa + o) | kLbo16, kHi32, (ka + o) | kLbo16, kHi32, idS, (N128 | blk) != 0);
+                    const uint32_t oq = (N128 * 16384 + blk * 4096) >> 4, ok = (N128 * G::kK128 + blk * G::kK32) >> 4;
+                    mma_ss1(d_s, (qa + oq) | kLbo16, kHi32, (ka + ok) | kLbo16, kHi32, idS, (N128 | blk) != 0);
                 }
             }
         };
         // O_t += P_t V: ncols / 16 K-steps of 16 keys, both tiles interleaved; A = P_t from TMEM
         auto issue_pv = [&](int vst, uint32_t accumulate, int ncols, bool two) {
-            const uint32_t va = v_lo + ((vst * G::kSlot) >> 4);
+            const uint32_t va = v_lo + ((vst * G::kSlotKV) >> 4);
             if (kKv / 16 == 7) {
                 const uint64_t dv = ((uint64_t)kHi32 << 32) | (va | kLboV);
                 mma_group_pv7(tmem + G::kOCol0, tmem + G::kOCol0 + G::kOStride, tmem + kPCol, tmem + kPCol + 64, dv,
@@ -742,7 +795,7 @@ int launch(const pab_attn_args* a, cudaStream_t st) {
             return launch_status("attn_fa smem attribute");
         attr_set = true;
     }
-    CUtensorMap mq128, mq32, mk128, mk32, mv32;
+    CUtensorMap mq128, mq32, mk128, mk32, mv32, mo;
     const CUtensorMapSwizzle big = N128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B;
     const int inner = N128 ? 64 : 16;
     if (!make_map(&mq128, a->q, a->dh, a->heads, a->n_q, a->n_b, a->n_a, a->q_si, a->q_sb, a->q_sa, inner, kRows, 1,
@@ -754,7 +807,10 @@ int launch(const pab_attn_args* a, cudaStream_t st) {
         !make_map(&mk32, a->k, a->dh, a->heads, a->n_k, a->n_b, a->n_a, a->k_si, a->k_sb, a->k_sa, 16, kKv, 1,
                   CU_TENSOR_MAP_SWIZZLE_32B) ||
         !make_map(&mv32, a->v, a->dh, a->heads, a->n_k, a->n_b, a->n_a, a->v_si, a->v_sb, a->v_sa, 16, kKv, 1,
-                  CU_TENSOR_MAP_SWIZZLE_32B))
+                  CU_TENSOR_MAP_SWIZZLE_32B) ||
+        // O rows leave through one TMA tensor store per 128-row tile (box = dh x 128 rows)
+        !make_map(&mo, a->o, a->dh, a->heads, a->n_q, a->n_b, a->n_a, a->o_si, a->o_sb, a->o_sa, a->dh, kRows, 1,
+                  CU_TENSOR_MAP_SWIZZLE_NONE))
         return PAB_ERR_CUDA;
     Params p;
     p.n_q = a->n_q;
@@ -782,7 +838,7 @@ int launch(const pab_attn_args* a, cudaStream_t st) {
         if (num_sms <= 0) num_sms = 148;
     }
     dim3 grid((unsigned)(p.n_items < num_sms ? p.n_items : num_sms));
-    attn_fa_kernel<N128, N32, NV><<<grid, kThreads, G::kSmem, st>>>(mq128, mq32, mk128, mk32, mv32, p);
+    attn_fa_kernel<N128, N32, NV><<<grid, kThreads, G::kSmem, st>>>(mq128, mq32, mk128, mk32, mv32, mo, p);
     return launch_status("attn_fa");
 }
 
