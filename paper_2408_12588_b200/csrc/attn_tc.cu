@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap q128, const __grid_constant__ CUtensorMap q32,
                    const __grid_constant__ CUtensorMap k128, const __grid_constant__ CUtensorMap k32,
                    const __grid_constant__ CUtensorMap v128, const __grid_constant__ CUtensorMap v32,
-                   const Params p) {
+                   const __grid_constant__ CUtensorMap omap, const Params p) {
     using G = Geometry<N128, N32>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     // ---------------------------------------------------------------- setup
     if (warp == kTmaWarp && lane == 0) {
-        prefetch_map(&q128); prefetch_map(&k128); prefetch_map(&v32);
+        prefetch_map(&q128); prefetch_map(&k128); prefetch_map(&v32); prefetch_map(&omap);
         if (N32) { prefetch_map(&q32); prefetch_map(&k32); }
         mbar_init(&bars->q_full, 1);
         mbar_init(&bars->q_empty, 2);  // both tiles' MMA warps are done with Q
@@ -424,6 +424,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t p_row = smem_u32(p_blk) + (uint32_t)row * 128u;
         const int total_iters = my_items * n_iter;
         int gi = 0;
+        const bool o_issuer = (hc == 0 && wl == 0 && lane == 0);  // issues this tile's O store
+        uint8_t* o_stage = smem + G::kP0 + t * kPBytes;           // dense O rows, staged in the P block
 
         for (int c = 0; c < my_items; ++c) {
             const Item it = decode((int)blockIdx.x + c * (int)gridDim.x);
@@ -455,6 +457,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int slot = gi & 1;
                 PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 2);
                 xch[(hc * 3 + slot) * kRows + row] = mx;
+                // the previous item's O tile store has finished reading its staging (the P block
+                // this group is about to overwrite) before the group passes this barrier
+                if (o_issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(kGroupThreads) : "memory");
                 mx = fmaxf(mx, xch[((1 - hc) * 3 + slot) * kRows + row]);
                 const float m_tile = mx * p.scale_log2;
@@ -523,41 +528,44 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float l_tot = l_run + xch[((1 - hc) * 3 + 2) * kRows + row];
             mbar_wait(&bars->o_done[t], (gi - 1) & 1);
             tc_fence_after();
-            bool store = false;
-            __nv_bfloat16* dst = nullptr;
-            if (p.packed) {
-                const int b = b_base(it, t) + group, i = row - group * T;
-                store = (group < p.packed) && (b < p.n_b) && (i < T);
-                dst = p.o + (int64_t)it.a_idx * p.o_sa + (int64_t)b * p.o_sb + (int64_t)i * p.o_si +
-                      (int64_t)it.h * p.dh;
-            } else {
-                const int i = i_base(it, t) + row;
-                store = i < p.n_q;
-                dst = p.o + (int64_t)it.a_idx * p.o_sa + (int64_t)b_base(it, t) * p.o_sb + (int64_t)i * p.o_si +
-                      (int64_t)it.h * p.dh;
-            }
+            // O rows leave through the tile's (now idle) P block and ONE asynchronous TMA tensor
+            // store per tile: plain row stores from every CTA at the same moment form a GPU-wide
+            // write burst the softmax stalls on (the same fix as attn_fa.cu's epilogue).
             const float inv = (l_tot > 0.f) ? 1.0f / l_tot : 0.f;
+            uint8_t* stg = o_stage + row * (2 * p.dh);  // dense rows: the TMA box layout
             for (int cc = c_lo; cc < c_hi; ++cc) {
                 float o[16];
                 PAB_TMEM_LD16(o_tmem + 16 * cc, o);
                 tmem_wait_ld();
-                if (store) {
 #pragma unroll
-                    for (int e = 0; e < 16; e += 8) {
-                        if (16 * cc + e < p.dh) {
-                            uint32_t w[4];
+                for (int e = 0; e < 16; e += 8) {
+                    if (16 * cc + e < p.dh) {
+                        uint32_t w[4];
 #pragma unroll
-                            for (int q = 0; q < 4; ++q)
-                                w[q] = pack_bf16(o[e + 2 * q] * inv, o[e + 2 * q + 1] * inv);
-                            *reinterpret_cast<uint4*>(dst + 16 * cc + e) = make_uint4(w[0], w[1], w[2], w[3]);
-                        }
+                        for (int q = 0; q < 4; ++q) w[q] = pack_bf16(o[e + 2 * q] * inv, o[e + 2 * q + 1] * inv);
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(stg + (16 * cc + e) * 2)),
+                                     "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                                     : "memory");
                     }
                 }
+            }
+            fence_async_smem();
+            asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(kGroupThreads) : "memory");
+            if (o_issuer) {
+                // packed: box (dh, 1, T, packed, 1) at (0, h, 0, first sequence, a); rows past the
+                // problem count / n_q are clipped by the tensor map
+                const int ci = p.packed ? 0 : i_base(it, t), cb = b_base(it, t);
+                asm volatile(
+                    "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];\n\t"
+                    "cp.async.bulk.commit_group;" ::"l"(reinterpret_cast<uint64_t>(&omap)),
+                    "r"(smem_u32(o_stage)), "r"(0), "r"(it.h), "r"(ci), "r"(cb), "r"(it.a_idx)
+                    : "memory");
             }
             // O may now be overwritten by the next item's first P.V
             tc_fence_before();
             mbar_arrive(&bars->o_free[t]);
         }
+        if (o_issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // O stores done before exit
     }
     __syncthreads();
     if (warp == kMmaWarp) {
@@ -610,7 +618,7 @@ int launch(const pab_attn_args* a, int packed, cudaStream_t st) {
     }
     const int box_i = packed ? a->n_k : kRows;
     const int box_b = packed ? packed : 1;
-    CUtensorMap maps[6];
+    CUtensorMap maps[7];
     struct Op { const void* ptr; int64_t sa, sb, si; int n_i; } ops[3] = {
         {a->q, a->q_sa, a->q_sb, a->q_si, a->n_q}, {a->k, a->k_sa, a->k_sb, a->k_si, a->n_k},
         {a->v, a->v_sa, a->v_sb, a->v_si, a->n_k}};
@@ -623,6 +631,10 @@ int launch(const pab_attn_args* a, int packed, cudaStream_t st) {
                       box_i, box_b, CU_TENSOR_MAP_SWIZZLE_32B))
             return PAB_ERR_CUDA;
     }
+    // O: one TMA tensor store per 128-row tile (box = dh x the Q box rows), no swizzle
+    if (!make_map(&maps[6], a->o, a->dh, a->heads, a->n_q, a->n_b, a->n_a, a->o_si, a->o_sb, a->o_sa, a->dh, box_i,
+                  box_b, CU_TENSOR_MAP_SWIZZLE_NONE))
+        return PAB_ERR_CUDA;
     Params p;
     p.n_q = a->n_q; p.n_k = a->n_k; p.n_b = a->n_b; p.heads = a->heads; p.dh = a->dh;
     p.packed = packed;
@@ -653,7 +665,7 @@ int launch(const pab_attn_args* a, int packed, cudaStream_t st) {
     }
     dim3 grid((unsigned)(p.n_items < num_sms ? p.n_items : num_sms));
     attn_tc_kernel<N128, N32><<<grid, kThreads, G::kSmem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4],
-                                                                 maps[5], p);
+                                                                 maps[5], maps[6], p);
     return launch_status("attn_tc");
 }
 
@@ -672,7 +684,7 @@ extern "C" int pab_attn_debug_trace(long long* device_buffer) {
 bool attn_tc_supported(const pab_attn_args* a) {
     if (a->dh % 8 != 0 || a->dh > 80 || a->n_k < 1) return false;  // smem: 7 operand tiles + 2 P tiles
     const int64_t strides[] = {a->q_sa, a->q_sb, a->q_si, a->k_sa, a->k_sb, a->k_si,
-                               a->v_sa, a->v_sb, a->v_si, a->o_si};
+                               a->v_sa, a->v_sb, a->v_si, a->o_sa, a->o_sb, a->o_si};  // all TMA-addressed
     for (int64_t s : strides)
         if (s % 8 != 0 || s < 0) return false;
     const uintptr_t ptrs[] = {(uintptr_t)a->q, (uintptr_t)a->k, (uintptr_t)a->v, (uintptr_t)a->o};
