@@ -115,6 +115,7 @@ struct Geometry {
 
 struct Bars {
     uint64_t q_full[2], q_empty[2], k_full[3], k_empty[3], v_full[3], v_ready[3], v_empty[3];
+    uint64_t q_ready[2], k_ready[3];  // Q / K tiles after the fixer warp's pad-column patch
     uint64_t s_full, s_free, p_full, o_done;  // shared by the two query tiles (they run in phase)
 };
 
@@ -251,8 +252,10 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
 // 1.5*2^23 magic constant, 2^f by a degree-3 minimax polynomial on [-0.5, 0.5]
 // (max rel err 7.5e-5, far below the bf16 rounding of P), exponent add as an integer.
 __device__ __forceinline__ void poly_exp2_x2(float& a, float& b) {
-    a = fmaxf(a, -127.0f);
-    b = fmaxf(b, -127.0f);
+    // clamp at -126: 2^f of the polynomial has biased exponent 126 for f < 0, so adding
+    // -127 << 23 would wrap the exponent field to 255 (NaN); -126 gives a denormal ~1e-38
+    a = fmaxf(a, -126.0f);
+    b = fmaxf(b, -126.0f);
     const unsigned long long x = f2_pack(a, b);
     const unsigned long long t = f2_add(x, f2_pack(12582912.0f, 12582912.0f));
     const unsigned long long j = f2_add(t, f2_pack(-12582912.0f, -12582912.0f));
@@ -327,6 +330,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int my_items = (p.n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
     const int n_kv = p.n_kv;
     const int n_iters = my_items * n_kv;  // global (item, kv tile) iterations of this CTA
+    // Pad-column key mask (dh % 16 != 0, e.g. 72): column dh of the zero-padded head dim is
+    // 1.0 in every Q row and -1e30 in the K rows past n_k, so the S MMA itself scores the
+    // padded keys of a partial last KV tile at -1e30 (exp -> 0, never the max): that tile
+    // runs the unmasked softmax over all 112 columns and full-width MMAs.
+    const bool padmask = N32 > 0 && (p.dh & 15) != 0;
 
     // ---------------------------------------------------------------- setup
     if (warp == kTmaWarp && lane == 0) {
@@ -340,10 +348,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&bars->q_full[s], 1);
+            mbar_init(&bars->q_ready[s], 1);
             mbar_init(&bars->q_empty[s], 1);
         }
         for (int s = 0; s < 3; ++s) {
             mbar_init(&bars->k_full[s], 1);
+            mbar_init(&bars->k_ready[s], 1);
             mbar_init(&bars->k_empty[s], 1);
             mbar_init(&bars->v_full[s], 1);
             mbar_init(&bars->v_ready[s], 1);
@@ -500,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->s_free);
                 FA_TRACE(trc, it_n, t, 2);
-                const bool masked = (j == n_kv - 1) && (tail < kHalf);
+                const bool masked = !padmask && (j == n_kv - 1) && (tail < kHalf);
                 if (masked) {
 #pragma unroll
                     for (int cc = 0; cc < kHalf; ++cc) s[cc] = (cc < tail) ? s[cc] : -INFINITY;
@@ -649,22 +659,52 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == kFixWarp) {
-        // ====================================== V fixer: V[:, dh] = 1 (zero-filled by TMA)
-        // the P.V MMA then accumulates the row sums into O[:, dh].
-        // SW32 atom layout: row r at 32 r, 16-byte chunk index XOR (r >> 2) & 1.
+        // ====================================== fixer warp (after each TMA load, before the MMA)
+        // V[:, dh] = 1 (zero-filled by TMA): the P.V MMA then accumulates the row sums into
+        // O[:, dh].  With padmask also Q[:, dh] = 1 and, in a partial last K tile, K[r, dh] =
+        // -1e30 for rows r >= the live keys (see padmask).
+        // SW32 atoms: row r at 32 r, 16-byte chunk index XOR (r >> 2) & 1.
         const int col = p.dh % 16;
         const uint32_t atom_off = (uint32_t)(p.dh / 16) * (uint32_t)G::kVAtom;
-        for (int g = 0; g < n_iters; ++g) {
-            const int st = g % 3;
-            mbar_wait(&bars->v_full[st], (g / 3) & 1);
-            uint8_t* vd = smem + G::kV0 + st * G::kSlotKV + atom_off;
-            for (int r = lane; r < kKv; r += 32) {
-                const uint32_t chunk = (uint32_t)(col >> 3) ^ (uint32_t)((r >> 2) & 1);
-                *reinterpret_cast<__nv_bfloat16*>(vd + r * 32 + chunk * 16 + (col & 7) * 2) = __float2bfloat16_rn(1.0f);
-            }
+        const uint32_t cw = (uint32_t)(col & 7) * 2;
+        auto sw32 = [&](int r) { return (uint32_t)r * 32u + (((uint32_t)(col >> 3) ^ (uint32_t)((r >> 2) & 1)) * 16u) + cw; };
+        const int blk = (p.dh - 64 * N128) >> 4;  // SW32 block of column dh in Q / K
+        const uint32_t q_off = (uint32_t)(N128 * 16384 + blk * 4096), k_off = (uint32_t)(N128 * G::kK128 + blk * G::kK32);
+        const int tail_k = p.n_k - (n_kv - 1) * kKv;
+#ifndef PAB_FA_PADK
+#define PAB_FA_PADK -1e30f
+#endif
+        const __nv_bfloat16 one = __float2bfloat16_rn(1.0f), neg = __float2bfloat16_rn(PAB_FA_PADK);
+        int g = 0;
+        for (int c = 0; c < my_items; ++c) {
+            const Item it = decode((int)blockIdx.x + c * (int)gridDim.x);
+            const int qb = c & 1;
+            mbar_wait(&bars->q_full[qb], (c >> 1) & 1);
+            if (padmask)
+                for (int t = 0; t < (it.two ? 2 : 1); ++t) {
+                    uint8_t* qd = smem + G::kQ0 + (2 * qb + t) * G::kSlot + q_off;
+                    for (int r = lane; r < kRows; r += 32) *reinterpret_cast<__nv_bfloat16*>(qd + sw32(r)) = one;
+                }
             fence_async_smem();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bars->v_ready[st]);
+            if (lane == 0) mbar_arrive(&bars->q_ready[qb]);
+            for (int j = 0; j < n_kv; ++j, ++g) {
+                const int st = g % 3;
+                mbar_wait(&bars->k_full[st], (g / 3) & 1);
+                if (padmask && j == n_kv - 1 && tail_k < kKv) {
+                    uint8_t* kd = smem + G::kK0 + st * G::kSlotKV + k_off;
+                    for (int r = tail_k + lane; r < kKv; r += 32) *reinterpret_cast<__nv_bfloat16*>(kd + sw32(r)) = neg;
+                }
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->k_ready[st]);
+                mbar_wait(&bars->v_full[st], (g / 3) & 1);
+                uint8_t* vd = smem + G::kV0 + st * G::kSlotKV + atom_off;
+                for (int r = lane; r < kKv; r += 32) *reinterpret_cast<__nv_bfloat16*>(vd + sw32(r)) = one;
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->v_ready[st]);
+            }
         }
     } else if (warp == kMmaWarp) {
         // ============================ MMA issuer (warp-converged; one elected lane issues the MMAs)
@@ -680,6 +720,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // V: MN-major SW32, 16-column atoms kVAtom B apart (LBO), 8-row groups 256 B apart (SBO)
         constexpr uint32_t kLboV = ((uint32_t)G::kVAtom >> 4) << 16;
         auto cols_of = [&](int j) {
+            if (padmask) return kKv;  // padded keys are scored -1e30 by the MMA itself
             const int n = min(kKv, p.n_k - j * kKv);
             return (n + 15) & ~15;
         };
@@ -734,7 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int c = 0, j = 0, g = 0;
         Item it = decode((int)blockIdx.x);
         if (my_items > 0) {
-            mbar_wait2(&bars->q_full[0], 0, &bars->k_full[0], 0);
+            mbar_wait2(&bars->q_ready[0], 0, &bars->k_ready[0], 0);
             tc_fence_after();
             issue_s(0, 0, cols_of(0), it.two);
             tc_commit(&bars->s_full);
@@ -752,8 +793,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const Item it1 = (c1 == c) ? it : decode((int)blockIdx.x + c1 * (int)gridDim.x);
                 const int g1 = g + 1;
                 FA_TRACE(lane == 0, gi, 0, 10);
-                if (j1 == 0) mbar_wait(&bars->q_full[c1 & 1], (c1 >> 1) & 1);
-                mbar_wait2(&bars->s_free, gi & 1, &bars->k_full[g1 % 3], (g1 / 3) & 1);
+                if (j1 == 0) mbar_wait(&bars->q_ready[c1 & 1], (c1 >> 1) & 1);
+                mbar_wait2(&bars->s_free, gi & 1, &bars->k_ready[g1 % 3], (g1 / 3) & 1);
                 tc_fence_after();
                 FA_TRACE(lane == 0, gi, 0, 8);
                 issue_s(c1 & 1, g1 % 3, cols_of(j1), it1.two);

@@ -142,9 +142,9 @@ __device__ __forceinline__ float fast_exp2(float x) {
 // MUFU.EX2): round-to-nearest via the 1.5*2^23 magic constant, then a degree-4
 // Taylor polynomial of 2^f on [-0.5, 0.5] (rel err < 5e-5, far below the bf16
 // rounding of P).  Used for a share of the scores so MUFU is not the only exp2
-// engine.  Inputs are clamped at -127 (x -> -inf gives ~0).
+// engine.  Inputs are clamped at -126 (x -> -inf gives a denormal ~1e-38).
 __device__ __forceinline__ float poly_exp2(float x) {
-    x = fmaxf(x, -127.0f);
+    x = fmaxf(x, -126.0f);  // not -127: the exponent add would wrap to NaN (see poly_exp2_x2)
     const float t = x + 12582912.0f;                 // 1.5 * 2^23: integer part lands in the low mantissa
     const int xi = __float_as_int(t) - 0x4B400000;   // round(x)
     const float f = x - (t - 12582912.0f);           // x - round(x) in [-0.5, 0.5]

@@ -115,6 +115,31 @@ def test_attention_rising_scores_rescale(impl):
     check_close(out, want, ("rising", impl))
 
 
+@pytest.mark.parametrize("impl", [kernels.IMPL_TCGEN05, kernels.IMPL_TC_SPLIT], ids=["tcgen05", "tc_split"])
+@pytest.mark.parametrize("S", [1000, 1560, 300])
+def test_attention_wide_score_spread(impl, S):
+    # scores spread over hundreds of log2 units inside one KV tile: exp2 arguments far below
+    # -126 must underflow to 0 on both the MUFU and the FMA-pipe polynomial path (a -127
+    # clamp made the polynomial's exponent add wrap to NaN), and the -1e30 pad-column key
+    # mask of a partial last tile must stay exact
+    g = torch.Generator(device=DEV).manual_seed(11)
+    H, dh = 2, 72
+    D = H * dh
+    q = torch.randn(S, D, device=DEV, generator=g)
+    k = torch.randn(S, D, device=DEV, generator=g) * 40.0
+    v = torch.randn(S, D, device=DEV, generator=g)
+    q, k, v = (x.to(torch.bfloat16) for x in (q, k, v))
+    out = torch.full((S, D), float("nan"), device=DEV, dtype=torch.bfloat16)
+    st = (S * D, 0, D)
+    a = kernels.attn_args(q, k, v, out, st, st, st, st, 1, 1, S, S, H, dh)
+    kernels.attention(a, impl)
+    torch.cuda.synchronize()
+    hv = lambda x: x.view(1, S, H, dh).transpose(1, 2)  # noqa: E731
+    want = ref_attention(hv(q), hv(k), hv(v)).transpose(1, 2).reshape(S, D)
+    assert torch.isfinite(out.float()).all()
+    check_close(out, want, ("spread", impl, S))
+
+
 @pytest.mark.parametrize("impl", IMPLS, ids=IMPL_IDS)
 @pytest.mark.parametrize("B,T,S,H,dh", [(2, 16, 100, 2, 72), (1, 8, 64, 2, 72), (1, 32, 40, 2, 72),
                                          (2, 4, 16, 4, 8), (1, 24, 30, 2, 16), (1, 16, 1560, 1, 72)])
