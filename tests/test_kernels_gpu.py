@@ -86,7 +86,7 @@ IMPL_IDS = ["tcgen05", "simt", "tc_split"]
 @pytest.mark.parametrize("B,T,S,H,dh", [(1, 2, 1024, 2, 72), (1, 1, 1560, 2, 72), (2, 1, 200, 3, 72),
                                          (1, 2, 16, 4, 8), (1, 1, 300, 2, 16), (1, 1, 129, 1, 64),
                                          (1, 1, 77, 2, 32), (1, 1, 100, 2, 56), (1, 8, 1024, 16, 72),
-                                         (1, 3, 1560, 16, 72)])
+                                         (1, 3, 1560, 16, 72), (1, 2, 3600, 16, 72)])  # C3, C5 frames
 def test_spatial_attention(impl, B, T, S, H, dh):
     if impl == kernels.IMPL_TC_SPLIT and dh == 56:
         pytest.skip("the split-row kernel has no dh 56 instantiation")
@@ -142,7 +142,8 @@ def test_attention_wide_score_spread(impl, S):
 
 @pytest.mark.parametrize("impl", IMPLS, ids=IMPL_IDS)
 @pytest.mark.parametrize("B,T,S,H,dh", [(2, 16, 100, 2, 72), (1, 8, 64, 2, 72), (1, 32, 40, 2, 72),
-                                         (2, 4, 16, 4, 8), (1, 24, 30, 2, 16), (1, 16, 1560, 1, 72)])
+                                         (2, 4, 16, 4, 8), (1, 24, 30, 2, 16), (1, 16, 1560, 1, 72),
+                                         (1, 32, 3600, 2, 72)])  # C5: 32 frames, 4 sequences per tile
 def test_temporal_attention(impl, B, T, S, H, dh):
     out, want, a = temporal_case(B, T, S, H, dh, impl)
     check_close(out, want, ("temporal", impl, B, T, S, H, dh))
@@ -150,7 +151,8 @@ def test_temporal_attention(impl, B, T, S, H, dh):
 
 @pytest.mark.parametrize("impl", IMPLS, ids=IMPL_IDS)
 @pytest.mark.parametrize("B,N,M,H,dh", [(2, 2048, 300, 2, 72), (2, 1000, 120, 2, 72), (1, 64, 16, 2, 72),
-                                         (2, 64, 8, 4, 8), (1, 500, 5, 2, 16), (2, 24960, 300, 16, 72)])
+                                         (2, 64, 8, 4, 8), (1, 500, 5, 2, 16), (2, 24960, 300, 16, 72),
+                                         (1, 115200, 300, 2, 72)])  # C5: 32 x 3600 queries
 def test_cross_attention(impl, B, N, M, H, dh):
     out, want, a = cross_case(B, N, M, H, dh, impl)
     check_close(out, want, ("cross", impl, B, N, M, H, dh))
