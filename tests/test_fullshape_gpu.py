@@ -44,6 +44,36 @@ def test_c3_layer_three_steps_with_broadcast_vs_oracle():
     assert np.isfinite(got[-1]).all()
 
 
+def test_c2_latte_layer_pab_steps_vs_oracle():
+    """C2 (Latte 16f 512^2) at full shape for one layer: D1152, H16, T16, S1024, M120,
+    no cross attention in the temporal block, CFG batch 2; 4 steps of a table that
+    broadcasts spatial/temporal/cross with different source steps (output broadcast)."""
+    cfg = ModelConfig(layers=1, hidden=1152, heads=16, frames=16, spatial_tokens=1024, text_tokens=120,
+                      cross_in_temporal=False)
+    params = init_model(cfg, seed=11)
+    src = np.zeros((4, 1, 4), dtype=np.int32)
+    for i in range(4):
+        src[i, 0] = i
+    src[2, 0, 0] = 1  # spatial reuses step 1
+    src[3, 0, 1] = 1  # temporal reuses step 1 at step 3
+    src[3, 0, 2] = 2  # cross reuses step 2
+    table = DecisionTable(src)
+    ids = np.arange(120) % 256
+    den = Denoiser(params, make_schedule(4), table, ids, guidance=True, guidance_scale=4.0)
+    z = torch.from_numpy(initial_latent(params, 11, 2)).cuda()
+    got = []
+    den.run(z, on_step=lambda i, zz: got.append(zz.cpu().numpy().copy()))
+    assert den.ctx.launches.sites_reused == 3
+    ocfg = orc.Cfg(1, 1152, 16, 16, 1024, 120, cross_in_temporal=False)
+    want = []
+    orc.sample(ocfg, orc.init_weights(ocfg, 11), orc.linear_timesteps(4), src, seed=11, text_ids=ids,
+               guidance=True, per_step=want)
+    for i, (g, w) in enumerate(zip(got, want)):
+        rel = np.linalg.norm(g.astype(np.float64) - w) / np.linalg.norm(w)
+        mx = np.abs(g - w).max() / np.abs(w).max()
+        assert rel < 3.5e-2 and mx < 5e-2, (i, rel, mx)  # CFG (g=4) tolerance
+
+
 def test_c5_spatial_attention_3600_tokens():
     B, S, H, dh = 2, 3600, 16, 72
     D = H * dh
