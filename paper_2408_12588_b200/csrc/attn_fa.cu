@@ -58,6 +58,10 @@ constexpr uint32_t kSCol = 0, kPCol = 384;
 #define PAB_FA_BULK_EPI 1   // O rows leave through smem staging + cp.async.bulk (0: direct stores)
 #endif
 
+#ifndef PAB_FA_LAG
+#define PAB_FA_LAG 2  // 1: tile 1's row max waits for tile 0's (lag = one max phase); 2: its exp waits for tile 0's exp
+#endif
+
 #ifndef PAB_FA_POLY_DIV
 #define PAB_FA_POLY_DIV 3   // one column pair in PAB_FA_POLY_DIV on the FMA pipe (0: MUFU only)
 #endif
@@ -489,6 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&bars->s_free);
+                    if (PAB_FA_LAG && kSplit == 1) asm volatile("bar.sync %0, 64;" ::"r"(3 + wl + 4 * (it_n & 1)) : "memory");
                     if (it_n > 0) mbar_wait(&bars->o_done, (it_n - 1) & 1);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&bars->p_full);
@@ -511,6 +516,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (lane == 0) mbar_arrive(&bars->s_free);
                 FA_TRACE(trc, it_n, t, 2);
                 const bool masked = !padmask && (j == n_kv - 1) && (tail < kHalf);
+                // lag token (warps wl of tile 0 and tile 1 share an SM sub-partition): tile 1 starts
+                // its ALU-bound row max only when tile 0's is done, so it overlaps tile 0's MUFU-bound
+                // exp; the shared s_free / p_full barriers absorb a lag of one phase.  Two named
+                // barriers alternate by iteration parity: tile 0 can reach iteration j + 1's token
+                // before tile 1 consumed j's, never j + 2's (that P store needs tile 1's p_full(j)).
+                // Barrier ids 3..10 (1 and 2 are the epilogue's per-tile barriers).
+                if (PAB_FA_LAG == 1 && kSplit == 1 && t == 1) asm volatile("bar.sync %0, 64;" ::"r"(3 + wl + 4 * (it_n & 1)) : "memory");
                 if (masked) {
 #pragma unroll
                     for (int cc = 0; cc < kHalf; ++cc) s[cc] = (cc < tail) ? s[cc] : -INFINITY;
@@ -532,6 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     asm volatile("bar.sync %0, %1;" ::"r"(xbar), "r"(64) : "memory");
                     mx = fmaxf(mx, xs[(1 - hc) * kRows + row]);
                 }
+                if (PAB_FA_LAG == 1 && kSplit == 1 && t == 0) asm volatile("bar.arrive %0, 64;" ::"r"(3 + wl + 4 * (it_n & 1)) : "memory");
                 const float m_tile = mx * p.scale_log2;
                 // both halves hold identical (m_tile, m_run) per row and take the same decisions
                 const bool need = m_tile > m_run + 8.0f;
@@ -560,6 +573,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float neg_m = -m_run;
                 const unsigned long long sc2 = f2_pack(p.scale_log2, p.scale_log2), nm2 = f2_pack(neg_m, neg_m);
                 uint32_t pk[kHalf / 2];
+                if (PAB_FA_LAG == 2 && kSplit == 1 && t == 1) asm volatile("bar.sync %0, 64;" ::"r"(3 + wl + 4 * (it_n & 1)) : "memory");
                 if (kSplit == 1) {
                     if (masked) {
                         exp_pack<true, 16>(s, 0, sc2, nm2, tail, pk);
@@ -581,6 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         exp_pack<false, 12>(s, 32, sc2, nm2, kHalf, pk + 16);
                     }
                 }
+                if (PAB_FA_LAG == 2 && kSplit == 1 && t == 0) asm volatile("bar.arrive %0, 64;" ::"r"(3 + wl + 4 * (it_n & 1)) : "memory");
                 FA_TRACE(trc, it_n, t, 4);
                 if (!waited && it_n > 0) {
                     mbar_wait(&bars->o_done, (it_n - 1) & 1);

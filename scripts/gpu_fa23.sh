@@ -1,0 +1,8 @@
+timeout -s KILL 300 python -m pytest tests/test_kernels_gpu.py -q -m gpu -x > gpurun_out/t_attn.log 2>&1; echo "attn tests rc=$?"; tail -1 gpurun_out/t_attn.log; grep -E "FAILED" gpurun_out/t_attn.log | head -3
+PAB_LIB_PATH=$PWD/_variants/lag2.so timeout -s KILL 300 python -m pytest tests/test_kernels_gpu.py -q -m gpu -x -k "spatial or cross" 2>&1 | tail -1
+for v in prod lag0 lag2 prod lag0 lag2; do
+  if [ $v = prod ]; then L=""; else L=$PWD/_variants/$v.so; fi
+  for cfg in C3 C5; do
+  echo "== $v $cfg"; PAB_LIB_PATH=$L timeout -s KILL 60 python scripts/bench_attn.py --config $cfg --impl 1 | python -c "import json,sys; d=json.load(sys.stdin); print({k: round(v.get('us'),1) for k,v in d.items()})"
+  done
+done
