@@ -48,6 +48,7 @@ from .model import (
     ModelParams,
     TraceRecord,
     embed_text,
+    embed_text_ids,
     timestep_embedding,
 )
 
@@ -111,6 +112,15 @@ class StepContext:
         # (L, 4, N, 2D) -> (N, L, 4, 2D)
         self.mods = torch.matmul(t_vecs[None, None], params.w_mod_all).permute(2, 0, 1, 3).contiguous()
 
+        # Batch rows whose text is all null (id -1 -> zero embedding, e.g. the unconditional CFG
+        # half) have K = V = 0 at every cross site, so the reference's cross output for them is
+        # exactly 0 (softmax of zero logits times zero values, model.py:376-385).  When those
+        # rows trail the batch, cross sites compute only the leading `cross_live` rows and
+        # write zeros for the rest -- bit-identical, half the cross work under CFG.
+        ids_arr = embed_text_ids(params.cfg, text_ids, batch)
+        null = [bool(np.all(ids_arr[b] < 0)) for b in range(batch)]
+        n_null = sum(null)
+        self.cross_live = batch - n_null if null[batch - n_null:] == [True] * n_null else batch
         # per-run constants: text K/V of every cross site (step invariant)
         emb = embed_text(params, text_ids, batch).to(torch.bfloat16).reshape(batch * self.M, D)
         self.text_kv = []
@@ -146,7 +156,7 @@ class StepContext:
                 kk, vv = kv[:, :D], kv[:, D:]
                 per.append(kernels.attn_args(
                     self.qbuf, kk, vv, self.attn_out, (T * S * D, 0, D), (M * 2 * D, 0, 2 * D),
-                    (M * 2 * D, 0, 2 * D), (T * S * D, 0, D), B, 1, T * S, M, H, dh))
+                    (M * 2 * D, 0, 2 * D), (T * S * D, 0, D), self.cross_live, 1, T * S, M, H, dh))
             self.args_cross.append(per)
 
 
@@ -393,11 +403,15 @@ class _Step:
 
         def compute(o):
             self.prologue(2)
-            torch.mm(c.h, p.wq, out=c.qbuf)
-            kernels.attention(c.args_cross[self._li][blk], c.attn_impl)
-            torch.mm(c.attn_out, p.wo, out=o)
-            c.launches.attention_calls += 1
-            c.launches.gemm_calls += 2
+            rl = c.cross_live * c.T * c.S  # rows with non-null text (see StepContext.build)
+            if rl:
+                torch.mm(c.h[:rl], p.wq, out=c.qbuf[:rl])
+                kernels.attention(c.args_cross[self._li][blk], c.attn_impl)
+                torch.mm(c.attn_out[:rl], p.wo, out=o[:rl])
+                c.launches.attention_calls += 1
+                c.launches.gemm_calls += 2
+            if rl < c.rows:
+                o[rl:].zero_()  # null-text rows: the exact cross output
             return o
 
         return compute
