@@ -121,6 +121,9 @@ class StepContext:
         null = [bool(np.all(ids_arr[b] < 0)) for b in range(batch)]
         n_null = sum(null)
         self.cross_live = batch - n_null if null[batch - n_null:] == [True] * n_null else batch
+        # scratch output of non-stored cross sites: only the live rows are ever written, so the
+        # null rows stay the zeros written here (no per-call memset)
+        self.o_scratch_cross = torch.zeros((self.rows, D), **bf) if self.cross_live < batch else None
         # per-run constants: text K/V of every cross site (step invariant)
         emb = embed_text(params, text_ids, batch).to(torch.bfloat16).reshape(batch * self.M, D)
         self.text_kv = []
@@ -404,14 +407,17 @@ class _Step:
         def compute(o):
             self.prologue(2)
             rl = c.cross_live * c.T * c.S  # rows with non-null text (see StepContext.build)
+            zeroed = False
+            if o is c.o_scratch and c.o_scratch_cross is not None:
+                o, zeroed = c.o_scratch_cross, True  # null rows are permanently zero
             if rl:
                 torch.mm(c.h[:rl], p.wq, out=c.qbuf[:rl])
                 kernels.attention(c.args_cross[self._li][blk], c.attn_impl)
                 torch.mm(c.attn_out[:rl], p.wo, out=o[:rl])
                 c.launches.attention_calls += 1
                 c.launches.gemm_calls += 2
-            if rl < c.rows:
-                o[rl:].zero_()  # null-text rows: the exact cross output
+            if rl < c.rows and not zeroed:
+                o[rl:].zero_()  # null-text rows: the exact cross output (cached outputs only)
             return o
 
         return compute
