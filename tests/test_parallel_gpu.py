@@ -77,7 +77,7 @@ def _worker(rank, world, port, guidance, split, q):
 
 
 @pytest.mark.parametrize("world,guidance,split", [(2, False, False), (2, True, False), (4, True, False),
-                                                  (2, True, True), (4, True, True)])
+                                                  (8, True, False), (2, True, True), (4, True, True)])
 def test_broadcast_sp_matches_serial(world, guidance, split):
     """split: CFG halves on two rank groups (reference split_batch, parallel.py:410-464)."""
     ctx = mp.get_context("spawn")
