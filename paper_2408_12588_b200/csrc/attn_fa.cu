@@ -14,7 +14,9 @@
 //   warps [4S, 8S)    the same for query tile 1
 //   warp  8S          MMA issuer (one elected lane issues the tcgen05.mma groups; owns TMEM)
 //   warp  8S + 1      TMA producer (lane 0)
-//   warp  8S + 2      V fixer (writes 1.0 into the first padded V column, see row sums)
+//   warp  8S + 2      fixer: 1.0 into the first padded V column (row sums) and, for
+//                     dh % 16 != 0, the pad-column key mask (Q[:, dh] = 1, K[pad rows, dh] =
+//                     -1e30, so partial last KV tiles need no masking in the softmax)
 //
 // TMEM (512 columns), KV tiles of 112 keys so that S, P and O of both tiles fit side by
 // side (no aliasing):  S_t [112t, 112t + 112),  O_t [224 + OC t, ...),  P_t [384 + 64t, +56).
@@ -29,6 +31,13 @@
 // when a tile's max exceeds it by more than 2^8, so P <= 256 and the rescale is rare.
 // exp2 runs on MUFU for most columns and on the FMA pipe (degree-3 polynomial on f32x2
 // pairs) for one pair in PAB_FA_POLY_DIV.
+//
+// Scheduling: the warps of tile 0 and tile 1 that share an SM sub-partition pass a token
+// (PAB_FA_LAG = 2) so their exp sections alternate while the other tile loads S, takes
+// its row max and stores P; the MMA groups still interleave both tiles' accumulators.
+// Epilogue: each item's O rows are staged densely in smem and leave through ONE TMA
+// tensor store per tile (an asynchronous bulk write instead of a GPU-wide burst of row
+// stores).  Measurements behind each choice: DESIGN.md section 8.1.
 #include "tc_ptx.cuh"
 
 namespace pab {
