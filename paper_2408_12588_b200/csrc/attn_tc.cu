@@ -59,7 +59,7 @@ struct Params {
     long long* trace;  // debug: clock64 event log of CTA (0,0,0), nullptr in production
 };
 
-// trace slot layout: [(j * 2 + t) * 16 + event]
+// trace slot layout: [(iteration * 2 + t) * 16 + event], iterations < 61 of CTA 0 (scripts/tc_timeline.py)
 #ifndef PAB_ATTN_TRACE
 #define PAB_TRACE(cond, j, t, ev) \
     do {                          \
@@ -431,10 +431,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const Item it = decode((int)blockIdx.x + c * (int)gridDim.x);
             float m_run = -INFINITY, l_run = 0.f;
             for (int j = 0; j < n_iter; ++j, ++gi) {
-                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 0);
+                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, gi < 60 ? gi : 60, t, 0);
                 mbar_wait(&bars->s_full[t], gi & 1);
                 tc_fence_after();
-                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 1);
+                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, gi < 60 ? gi : 60, t, 1);
                 // live score columns [lo, hi) of this row in this S tile
                 int lo = 0, hi = kKv;
                 if (p.packed) {
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                   : -INFINITY;
                 // exchange with the other column half of the same rows (double-buffered slot)
                 const int slot = gi & 1;
-                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 2);
+                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, gi < 60 ? gi : 60, t, 2);
                 xch[(hc * 3 + slot) * kRows + row] = mx;
                 // the previous item's O tile store has finished reading its staging (the P block
                 // this group is about to overwrite) before the group passes this barrier
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(kGroupThreads) : "memory");
                 mx = fmaxf(mx, xch[((1 - hc) * 3 + slot) * kRows + row]);
                 const float m_tile = mx * p.scale_log2;
-                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 3);
+                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, gi < 60 ? gi : 60, t, 3);
                 // previous P.V must be finished before P smem is overwritten or O rescaled
                 // (j == 0: the previous item's epilogue already waited for its last P.V)
                 if (j > 0) {
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     m_run = m_new;
                 }
                 const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
-                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 4);
+                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, gi < 60 ? gi : 60, t, 4);
                 // ---- pass 2: P = exp2(s * scale_log2 - m) -> bf16 into this half's 128B-swizzled P block.
                 // All 64 scores are pulled from TMEM first so S can be released (s_free) and the
                 // tensor pipe can start S(j+1) while this warp is still exponentiating.
@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 PAB_TMEM_LD32(s_tmem, v);
                 PAB_TMEM_LD32(s_tmem + 32, (v + 32));
                 tmem_wait_ld();
-                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 6);
+                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, gi < 60 ? gi : 60, t, 6);
                 tc_fence_before();
                 mbar_arrive(&bars->s_free[t]);
 #ifndef PAB_NO_MUFU_TOKEN
@@ -515,14 +515,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (t == 0 || gi + 1 < total_iters)
                     asm volatile("bar.arrive %0, %1;" ::"r"(4 - t), "r"(2 * kGroupThreads) : "memory");
 #endif
-                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 7);
+                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, gi < 60 ? gi : 60, t, 7);
                 l_run += psum;
                 fence_async_smem();
-                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, j, t, 5);
+                PAB_TRACE(wl == 0 && lane == 0 && hc == 0, gi < 60 ? gi : 60, t, 5);
                 mbar_arrive(&bars->p_full[t]);
             }
 
             // ------------------------------------------------------ epilogue of this item
+            PAB_TRACE(wl == 0 && lane == 0 && hc == 0, (gi - 1) < 60 ? (gi - 1) : 60, t, 8);
             xch[(hc * 3 + 2) * kRows + row] = l_run;
             asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(kGroupThreads) : "memory");
             const float l_tot = l_run + xch[((1 - hc) * 3 + 2) * kRows + row];
@@ -562,6 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     : "memory");
             }
             // O may now be overwritten by the next item's first P.V
+            PAB_TRACE(wl == 0 && lane == 0 && hc == 0, (gi - 1) < 60 ? (gi - 1) : 60, t, 9);
             tc_fence_before();
             mbar_arrive(&bars->o_free[t]);
         }
