@@ -424,7 +424,8 @@ def main():
     flops_pab, _ = video_flops(cfg, table, c["batch"])
 
     if rank == 0:
-        base = None if args.no_cpu_baseline else cpu_baseline(c)
+        # the CPU reference beside the GPU number: rank 0 at N=1 only (the scaling runs skip it)
+        base = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(c)
         line = {
             "metric": METRIC, "value": ms / 1000.0, "unit": "s/video", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
