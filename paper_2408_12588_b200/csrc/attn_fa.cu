@@ -71,6 +71,10 @@ constexpr uint32_t kSCol = 0, kPCol = 384;
 #define PAB_FA_LAG 2  // 1: tile 1's row max waits for tile 0's (lag = one max phase); 2: its exp waits for tile 0's exp
 #endif
 
+#ifndef PAB_FA_SINGLES_LAST
+#define PAB_FA_SINGLES_LAST 1  // single-tile items (odd tile count) scheduled last
+#endif
+
 #ifndef PAB_FA_POLY_DIV
 #define PAB_FA_POLY_DIV 3   // one column pair in PAB_FA_POLY_DIV on the FMA pipe (0: MUFU only)
 #endif
@@ -328,12 +332,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         int h, a_idx, b_idx, tile0;
         bool two;  // second query tile exists
     };
+    // With an odd tile count the last pair of every (problem, head) has a single query tile
+    // and costs ~0.7 of a two-tile item: those items are numbered last, so the tail round of
+    // the static CTA assignment holds the cheap ones.
+    const int n_full = PAB_FA_SINGLES_LAST ? p.row_tiles / 2 : p.n_pairs;  // pairs with two tiles first
+    const int items_full = n_full * p.heads * (p.n_items / (p.n_pairs * p.heads));
     auto decode = [&](int item) {
         Item it;
-        it.h = item % p.heads;
-        const int rest = item / p.heads;
-        const int pair = rest % p.n_pairs;
-        const int az = rest / p.n_pairs;
+        int pair, az;
+        if (item >= items_full) {  // single-tile items (pair n_full) of every (problem, head)
+            const int rest = item - items_full;
+            it.h = rest % p.heads;
+            az = rest / p.heads;
+            pair = n_full;
+        } else {
+            it.h = item % p.heads;
+            const int rest = item / p.heads;
+            pair = rest % n_full;
+            az = rest / n_full;
+        }
         it.a_idx = az / p.n_b;
         it.b_idx = az - it.a_idx * p.n_b;
         it.tile0 = 2 * pair;
