@@ -113,6 +113,14 @@ int pab_ddim_cfg(float* z, const float* r, const void* const* pending, int n_pen
 int pab_softmax_rows(const float* logits, int64_t ld_l, void* p_bf16, int64_t ld_p, int64_t rows, int64_t n,
                      float scale, void* stream);
 
+/*
+ * y = x + a * w on fp32 vectors (one rounding per element; y may alias x).
+ * Replaces the Delta-DiT whole-layer residual delta of forward_step, kept in
+ * fp32 like the reference: store d = x - x_layer_in (a = -1), replay x + d
+ * (a = 1) (pkg/src/pab_engine/model.py:506-523, 565-566).
+ */
+int pab_add_scaled_f32(float* y, const float* x, const float* w, float a, int64_t n, void* stream);
+
 /* tanh-approximation GELU on bf16 (numerics.py:154-158), in may equal out. */
 int pab_gelu_bf16(const void* in, void* out, int64_t n, void* stream);
 

@@ -15,6 +15,15 @@ reference, all below the bf16 tolerance the GPU path is held to:
   * broadcast_object="scores" (score replay, model.py:325-392, 476-493) keeps
     the probabilities in float32 like the reference.
 Decision tables are integer work and are restated exactly.
+
+bf16 emulation (``emulate_bf16=True`` on ``sample``/``forward``): every matmul
+operand and output is rounded to bf16 (round-to-nearest-even) where the B200
+path stores bf16 -- LN/modulate output h, weights, q/k/v, unnormalised softmax
+numerators P (the row sum is taken over the rounded P, as the kernels sum P
+through a ones column of V), attention output, GELU hidden, site output o, text
+embedding and its K/V -- while the residual stream, accumulations and the DDIM
+update stay fp32.  It measures the precision floor of a correct bf16 pipeline
+(SURVEY.md 8c), which is what the guided (CFG) parity gates are set against.
 """
 
 from __future__ import annotations
@@ -104,6 +113,18 @@ def init_weights(cfg: Cfg, seed: int) -> dict:
     return w
 
 
+def bf16_round(a):
+    """Round fp32 values to the nearest bf16 (ties to even), returned as fp32."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return r.view(np.float32)
+
+
+def _ident(a):
+    return a
+
+
 def _ln(x, eps=1e-5):
     # population variance, eps inside the sqrt (numerics.py:115-130)
     mu = x.mean(-1, keepdims=True)
@@ -116,10 +137,14 @@ def _softmax(z):
     return e / e.sum(-1, keepdims=True)
 
 
-def attention(q, k, v):
-    """softmax(q k^T / sqrt(dh)) v over the last two axes (numerics.py:133-151)."""
+def attention(q, k, v, rb=None):
+    """softmax(q k^T / sqrt(dh)) v over the last two axes (numerics.py:133-151).
+    rb: bf16 rounding of the unnormalised probabilities (emulation mode)."""
     s = np.matmul(q, np.swapaxes(k, -1, -2)) * np.float32(1.0 / math.sqrt(q.shape[-1]))
-    return np.matmul(_softmax(s), v)
+    if rb is None:
+        return np.matmul(_softmax(s), v)
+    e = rb(np.exp(s - s.max(-1, keepdims=True)))
+    return np.matmul(e, v) / e.sum(-1, keepdims=True)
 
 
 def _heads(x, h):
@@ -143,34 +168,36 @@ def time_embedding(t, d):
     return np.concatenate([np.sin(t * f), np.cos(t * f)])
 
 
-def site_output(cfg: Cfg, w: dict, li: int, kind: str, block: str, x, tvec, text):
-    """Post-projection, pre-residual output of one site (model.py:346-403)."""
+def site_output(cfg: Cfg, w: dict, li: int, kind: str, block: str, x, tvec, text, rb=None):
+    """Post-projection, pre-residual output of one site (model.py:346-403).
+    rb: bf16 rounding (emulation mode; weights in ``w`` are then already rounded)."""
     d = cfg.D
+    r = _ident if rb is None else rb
 
     def modnorm(mod_w):
         mod = tvec @ mod_w
-        return _ln(x) * (1.0 + mod[d:]) + mod[:d]
+        return r(_ln(x) * (1.0 + mod[d:]) + mod[:d])
 
     if kind == "mlp":
         p = f"{li}.{'ms' if block == 's' else 'mt'}"
         h = modnorm(w[p + ".mod"])
-        return _gelu(h @ w[p + ".w1"]) @ w[p + ".w2"]
+        return r(r(_gelu(h @ w[p + ".w1"])) @ w[p + ".w2"])
     if kind == "cross":
         p = f"{li}.{'cs' if block == 's' else 'ct'}"
         b, t, s, _ = x.shape
-        q = (x @ w[p + ".q"]).reshape(b, t * s, d)
-        k, v = text @ w[p + ".k"], text @ w[p + ".v"]
-        o = _unheads(attention(_heads(q, cfg.H), _heads(k, cfg.H), _heads(v, cfg.H)))
-        return o.reshape(b, t, s, d) @ w[p + ".o"]
+        q = r(r(x) @ w[p + ".q"]).reshape(b, t * s, d)
+        k, v = r(text @ w[p + ".k"]), r(text @ w[p + ".v"])
+        o = r(_unheads(attention(_heads(q, cfg.H), _heads(k, cfg.H), _heads(v, cfg.H), rb)))
+        return r(o.reshape(b, t, s, d) @ w[p + ".o"])
     p = f"{li}.{'sa' if kind == 'spatial' else 'ta'}"
     h = modnorm(w[p + ".mod"])
-    q, k, v = (h @ w[p + "." + n] for n in "qkv")
+    q, k, v = (r(h @ w[p + "." + n]) for n in "qkv")
     if kind == "temporal":
         q, k, v = (a.transpose(0, 2, 1, 3) for a in (q, k, v))
-    o = _unheads(attention(_heads(q, cfg.H), _heads(k, cfg.H), _heads(v, cfg.H)))
+    o = r(_unheads(attention(_heads(q, cfg.H), _heads(k, cfg.H), _heads(v, cfg.H), rb)))
     if kind == "temporal":
         o = o.transpose(0, 2, 1, 3)
-    return o @ w[p + ".o"]
+    return r(o @ w[p + ".o"])
 
 
 def _probs(q, k):
@@ -235,9 +262,10 @@ def stores_of(table: np.ndarray) -> set:
     return out
 
 
-def forward(cfg, w, x, t, text, table, step, cache, log=None, delta_mode=False, scores=False):
+def forward(cfg, w, x, t, text, table, step, cache, log=None, delta_mode=False, scores=False, rb=None):
     """One step (model.py:425-568); cache maps site -> (source step, value).
-    scores: broadcast_object="scores" (attention sites cache probabilities)."""
+    scores: broadcast_object="scores" (attention sites cache probabilities).
+    rb: bf16 rounding function (emulation mode, see module docstring)."""
     tvec = time_embedding(t, cfg.D).astype(np.float32) @ w["time"]
     stores = stores_of(table) if not delta_mode else None
     for li in range(cfg.L):
@@ -259,7 +287,7 @@ def forward(cfg, w, x, t, text, table, step, cache, log=None, delta_mode=False, 
                     o, probs = site_scores(cfg, w, li, kind, block, x, tvec, text)
                     cache[key] = (step, probs)
                 else:
-                    o = site_output(cfg, w, li, kind, block, x, tvec, text)
+                    o = site_output(cfg, w, li, kind, block, x, tvec, text, rb)
                     if stored:
                         cache[key] = (step, o)
                 dec = "compute"
@@ -289,19 +317,31 @@ def latent0(cfg: Cfg, seed: int, batch: int):
     return np.tile(z, (batch, 1, 1, 1))
 
 
+def bf16_weights(w: dict) -> dict:
+    """Matmul weights rounded to bf16 as the device holds them (modulation, time
+    and text tables stay fp32 like the device's; the text embedding is rounded
+    where it enters the K/V projection)."""
+    return {k: (v if k in ("time", "text") or k.endswith(".mod") else bf16_round(v)) for k, v in w.items()}
+
+
 def sample(cfg, w, timesteps, table, seed, text_ids=None, guidance=False, g=4.0, delta_mode=False,
-           per_step=None, log=None, scores=False):
-    """DDIM eta=0 sampler with optional CFG pair (diffusion.py:125-189)."""
+           per_step=None, log=None, scores=False, emulate_bf16=False):
+    """DDIM eta=0 sampler with optional CFG pair (diffusion.py:125-189).
+    emulate_bf16: bf16 operand/output rounding (module docstring)."""
     ab = alpha_bar_fn()
     batch = 2 if guidance else 1
     ids = np.arange(cfg.M) % 256 if text_ids is None else np.asarray(text_ids)
     ids2 = np.stack([ids, np.full_like(ids, -1)]) if guidance else ids[None]
     text = text_embedding(w, ids2)
+    rb = None
+    if emulate_bf16:
+        assert not scores, "bf16 emulation covers output broadcast"
+        rb, w, text = bf16_round, bf16_weights(w), bf16_round(text)
     x = latent0(cfg, seed, batch)
     cache: dict = {}
     n = len(timesteps)
     for i, t in enumerate(timesteps):
-        eps = forward(cfg, w, x, t, text, table, i, cache, log=log, delta_mode=delta_mode, scores=scores)
+        eps = forward(cfg, w, x, t, text, table, i, cache, log=log, delta_mode=delta_mode, scores=scores, rb=rb)
         if guidance:
             eps = eps[1:2] + np.float32(g) * (eps[0:1] - eps[1:2])
         a, an = ab(t), (ab(timesteps[i + 1]) if i + 1 < n else 1.0)

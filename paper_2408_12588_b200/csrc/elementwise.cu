@@ -468,6 +468,33 @@ extern "C" int pab_softmax_rows(const float* logits, int64_t ld_l, void* p_bf16,
     return launch_status("softmax_rows");
 }
 
+// y = x + a * w (fp32, 4 elements per thread): the Delta-DiT whole-layer residual
+// delta in fp32 (store: d = x_layer_out - x_layer_in, a = -1; replay: x += d, a = 1)
+__global__ void __launch_bounds__(256) add_scaled_f32_kernel(float* __restrict__ y, const float* __restrict__ x,
+                                                             const float* __restrict__ w, float a, int64_t n) {
+    const int64_t i4 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (i4 + 4 <= n) {
+        const float4 xv = *reinterpret_cast<const float4*>(x + i4);
+        const float4 wv = *reinterpret_cast<const float4*>(w + i4);
+        *reinterpret_cast<float4*>(y + i4) =
+            make_float4(__fmaf_rn(a, wv.x, xv.x), __fmaf_rn(a, wv.y, xv.y), __fmaf_rn(a, wv.z, xv.z),
+                        __fmaf_rn(a, wv.w, xv.w));
+    } else {
+        for (int64_t i = i4; i < n; ++i) y[i] = __fmaf_rn(a, w[i], x[i]);
+    }
+}
+
+extern "C" int pab_add_scaled_f32(float* y, const float* x, const float* w, float a, int64_t n, void* stream) {
+    if (n < 0) return PAB_ERR_SHAPE;
+    if (n == 0) return PAB_OK;
+    if (!y || !x || !w) return PAB_ERR_INVALID;
+    if ((uintptr_t)y % 16 || (uintptr_t)x % 16 || (uintptr_t)w % 16) return PAB_ERR_UNSUPPORTED;
+    const int64_t threads = (n + 3) / 4;
+    add_scaled_f32_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        y, x, w, a, n);
+    return launch_status("add_scaled_f32");
+}
+
 extern "C" int pab_gelu_bf16(const void* in, void* out, int64_t n, void* stream) {
     if (n < 0) return PAB_ERR_SHAPE;
     if (n == 0) return PAB_OK;

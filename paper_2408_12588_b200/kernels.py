@@ -152,6 +152,18 @@ def softmax_rows(logits: torch.Tensor, p_out: torch.Tensor, scale: float) -> tor
     return p_out
 
 
+def add_scaled_(y: torch.Tensor, x: torch.Tensor, w: torch.Tensor, a: float) -> torch.Tensor:
+    """y <- x + a * w (fp32, contiguous, equal sizes)."""
+    lib = _lib.load()
+    for t, name in ((y, "y"), (x, "x"), (w, "w")):
+        _need(t, torch.float32, name)
+        if not t.is_contiguous() or t.numel() != y.numel():
+            raise ShapeError("add_scaled operands must be contiguous and equally sized")
+    _lib.check(lib.pab_add_scaled_f32(y.data_ptr(), x.data_ptr(), w.data_ptr(), float(a), y.numel(), _stream()),
+               "pab_add_scaled_f32")
+    return y
+
+
 def gelu_(x: torch.Tensor) -> torch.Tensor:
     lib = _lib.load()
     _need(x, torch.bfloat16, "gelu input")

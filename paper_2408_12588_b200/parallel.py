@@ -186,6 +186,77 @@ def comm_volume_model(method: str, cfg, schedule, table: DecisionTable, workers:
     return rep
 
 
+# ---------------------------------------------------------------- logical workers
+class _LocalGroupState:
+    """Shared state of one in-process group of logical workers (threads)."""
+
+    def __init__(self, size: int):
+        import threading
+
+        self.size = size
+        self.barrier = threading.Barrier(size, timeout=600)
+        self.slots = [None] * size
+
+
+class LocalGroup:
+    """One logical worker's view of an in-process group.
+
+    The reference runs its W workers sequentially in one process
+    (parallel.py:1-15, 372-464); without a torch.distributed group,
+    ``run_parallel`` runs them as W threads on one GPU and exchanges shards
+    through this group: every member posts its send buffer, waits at a barrier,
+    copies its chunks from the peers' buffers and waits again before any buffer
+    can be rewritten.  All threads enqueue on the device's default stream, so
+    the copies are ordered after the producing kernels by issue order."""
+
+    def __init__(self, state: _LocalGroupState, rank: int):
+        self.state, self.rank = state, rank
+
+    def size(self) -> int:
+        return self.state.size
+
+    def _post(self, t):
+        st = self.state
+        st.slots[self.rank] = t
+        try:
+            st.barrier.wait()
+        except Exception:
+            st.barrier.abort()
+            raise
+
+    def _done(self):
+        st = self.state
+        try:
+            st.barrier.wait()
+        except Exception:
+            st.barrier.abort()
+            raise
+
+    def all_to_all_single(self, recv, send):
+        """send (W, ...) by destination -> recv (W, ...) by source."""
+        self._post(send)
+        W = self.state.size
+        rv, me = recv.view(W, -1), self.rank
+        for src in range(W):
+            rv[src].copy_(self.state.slots[src].reshape(W, -1)[me])
+        self._done()
+
+    def all_gather(self, t):
+        self._post(t)
+        parts = [p.clone() for p in self.state.slots]
+        self._done()
+        return parts
+
+    def all_gather_into(self, out, t):
+        self._post(t)
+        for dst, part in zip(out, self.state.slots):
+            dst.copy_(part.view_as(dst))
+        self._done()
+
+    def abort(self):
+        self.state.barrier.abort()
+
+
 # ---------------------------------------------------------------- exchange
 def send_order(h_shard, n_w: int):
     """Reference layout transform the CUDA prologue fuses: (B, T/W, S, D) ->
@@ -200,6 +271,9 @@ def _all_to_all(recv, send, group):
     all-to-all, so device tensors are staged through host memory there."""
     import torch.distributed as dist
 
+    if isinstance(group, LocalGroup):
+        group.all_to_all_single(recv, send)
+        return
     if send.is_cuda and dist.get_backend(group) == "gloo":
         host = recv.cpu()
         dist.all_to_all_single(host, send.cpu(), group=group)
@@ -212,6 +286,8 @@ def _all_gather(t, group=None):
     import torch
     import torch.distributed as dist
 
+    if isinstance(group, LocalGroup):
+        return group.all_gather(t)
     world = dist.get_world_size(group)
     if t.is_cuda and dist.get_backend(group) == "gloo":
         parts = [torch.empty_like(t, device="cpu") for _ in range(world)]
@@ -226,6 +302,9 @@ def _all_gather_into(out, t, group=None):
     """out (world, *t.shape) <- t of every rank of `group`, in group-rank order."""
     import torch.distributed as dist
 
+    if isinstance(group, LocalGroup):
+        group.all_gather_into(out, t)
+        return
     if t.is_cuda and dist.get_backend(group) == "gloo":
         for dst, part in zip(out, _all_gather(t.contiguous(), group)):
             dst.copy_(part.view_as(dst))
@@ -383,6 +462,9 @@ class ShardedDenoiser:
         if self._r is None or self._r.shape != z.shape:
             self._r = torch.empty_like(z)
         split = self.half is not None
+        # ledger and decision log describe the latest run (a long-lived server does not accumulate)
+        self.ledger.entries.clear()
+        self.ctx.launches.log.clear()
         if split and (self._pair is None or self._pair[0].shape[1:] != z.shape[1:]):
             # (2, T/W, S, D) pair buffers: eps of both halves, latent slot per half
             self._pair = (torch.empty((2, *z.shape[1:]), device=z.device, dtype=z.dtype),
@@ -413,14 +495,23 @@ class ShardedDenoiser:
     def __call__(self, x_host, out=None):
         """Serving call on this rank: H2D of its frames (of its CFG half under
         split_batch) of the pinned host latent, denoise, D2H into `out` (or a new tensor)."""
+        import torch
+
         n = self.plan.frames_per_worker
         sl = slice(self.rank * n, (self.rank + 1) * n)
-        bl = slice(None) if self.half is None else slice(self.half, self.half + 1)
-        z = x_host[bl, sl].to(self.params.w_time.device, non_blocking=True)
+        bs = range(x_host.shape[0]) if self.half is None else [self.half]
+        dev = self.params.w_time.device
+        z = torch.empty((len(bs), n, *x_host.shape[2:]), device=dev, dtype=x_host.dtype)
+        # x_host[b, frames] is contiguous: one async H2D per batch entry straight from the
+        # caller's (pinned) buffer, no host-side gather of the strided frame slice
+        for j, b in enumerate(bs):
+            z[j].copy_(x_host[b, sl], non_blocking=True)
         self.run(z)
         if out is None:
             return z.cpu()
-        out[bl, sl].copy_(z, non_blocking=True)
+        for j, b in enumerate(bs):
+            out[b, sl].copy_(z[j], non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()  # `out` is host memory: valid on return
         return out
 
 
@@ -506,8 +597,10 @@ def run_parallel(
 
     Every rank of an initialised torch.distributed group of size ``workers``
     calls this collectively (one process per GPU, NCCL); each returns the
-    gathered full latent.  ``workers == 1`` without a process group runs the
-    single-GPU engine.
+    gathered full latent.  Without a process group, ``workers`` logical
+    workers run in this process on the current GPU, as the reference runs
+    them (one thread per worker, shards exchanged through ``LocalGroup``);
+    ``workers == 1`` is the single-GPU engine.
     """
     import torch
     import torch.distributed as dist
@@ -522,6 +615,9 @@ def run_parallel(
     if text_ids is None:
         text_ids = default_text_ids(params)
     multi = dist.is_available() and dist.is_initialized()
+    if not multi and workers > 1:
+        return _run_logical(params, schedule, table, text_ids, workers, method, seed, guidance, guidance_scale,
+                            split_batch, noise_params, bytes_per_element)
     world = dist.get_world_size() if multi else 1
     rank = dist.get_rank() if multi else 0
     if workers != world:
@@ -555,4 +651,62 @@ def run_parallel(
     res._batch = den.batch
     res._tail = (cfg.spatial_tokens, cfg.hidden)
     res._split_gw = world // 2 if use_split else None
+    return res
+
+
+def _run_logical(params, schedule, table, text_ids, workers, method, seed, guidance, guidance_scale, split_batch,
+                 noise_params, bytes_per_element) -> ParallelRunResult:
+    """W logical workers on this process's GPU (threads exchanging through LocalGroup)."""
+    import threading
+
+    import torch
+
+    cfg = params.cfg
+    plan_shards(workers, cfg)
+    use_split = bool(split_batch and guidance and workers % 2 == 0)
+    dev = params.w_time.device
+    batch = 2 if guidance else 1
+    x_full = torch.from_numpy(initial_latent(params, seed, batch)).to(dev)
+    gw = workers // 2 if use_split else workers
+    sp = [_LocalGroupState(gw) for _ in range(2 if use_split else 1)]
+    pairs = [_LocalGroupState(2) for _ in range(gw)] if use_split else []
+    dens, outs, errs = [None] * workers, [None] * workers, []
+
+    def worker(w):
+        try:
+            torch.cuda.set_device(dev)
+            half, r = divmod(w, gw)
+            kw = dict(guidance=guidance, guidance_scale=guidance_scale, rank=r, world=gw,
+                      group=LocalGroup(sp[half], r), method=method, noise_params=noise_params,
+                      bytes_per_element=bytes_per_element)
+            if use_split:
+                kw.update(half=half, cfg_group=LocalGroup(pairs[r], half), total_workers=workers)
+            den = ShardedDenoiser(params, schedule, table, text_ids, **kw)
+            dens[w] = den
+            z = den.shard_input(x_full[half:half + 1] if use_split else x_full)
+            den.run(z)
+            outs[w] = z
+        except BaseException as e:  # noqa: BLE001 - re-raised on the calling thread
+            errs.append(e)
+            for st in sp + pairs:
+                st.barrier.abort()
+
+    threads = [threading.Thread(target=worker, args=(w,), name=f"pab-worker-{w}") for w in range(workers)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errs:
+        real = [e for e in errs if not isinstance(e, threading.BrokenBarrierError)]
+        raise (real or errs)[0]
+    torch.cuda.synchronize(dev)
+    if use_split:
+        latent = torch.cat([torch.cat(outs[:gw], dim=1), torch.cat(outs[gw:], dim=1)], dim=0)
+    else:
+        latent = torch.cat(outs, dim=1)
+    res = ParallelRunResult(latent=latent.cpu().numpy(), comm_report=dens[0].ledger, plan=dens[0].plan,
+                            worker_caches=[d.cache for d in dens])
+    res._batch = dens[0].batch
+    res._tail = (cfg.spatial_tokens, cfg.hidden)
+    res._split_gw = gw if use_split else None
     return res

@@ -133,7 +133,15 @@ class StepContext:
             self.text_kv.append((kv_s, kv_t))
 
         self._build_attention_args()
+        self._delta_in = None
         return self
+
+    def delta_in(self, r):
+        """Copy of the residual at a Delta-DiT layer input (one reused fp32 buffer)."""
+        if self._delta_in is None or self._delta_in.shape != r.shape:
+            self._delta_in = torch.empty_like(r)
+        self._delta_in.copy_(r)
+        return self._delta_in
 
     def _build_attention_args(self):
         B, T, S, D, H, dh, M = self.B, self.T, self.S, self.D, self.H, self.dh, self.M
@@ -445,7 +453,10 @@ class _Step:
             entry = self.cache.fetch((li, None, "delta"), "delta")
             if entry.source_step != source:
                 raise PolicyError(f"delta cache for layer {li} holds step {entry.source_step}, table expects {source}")
-            self.pending.append(entry.value)
+            # the fp32 delta is added to the materialised residual (reference keeps it fp32)
+            self.flush()
+            kernels.add_scaled_(self.r, self.r, entry.value, 1.0)
+            self.ctx.launches.other_calls += 1
             sites = [(SP, "s"), (CR, "s"), (ML, "s"), (TM, "t"), (ML, "t")]
             if self.ctx.cfg.cross_in_temporal:
                 sites.insert(4, (CR, "t"))
@@ -453,9 +464,9 @@ class _Step:
                 self.record(li, kind, block, "delta", d.source(li, kind), None)
             return
         x_in = None
-        if delta:
+        if delta and d.should_store_delta(li):
             self.flush()
-            x_in = self.r.clone()
+            x_in = self.ctx.delta_in(self.r)
         sc = self.ctx.broadcast_object == "scores"
         self.run_site(li, SP, "s", self.attn_site(lp.spatial, MOD_SPATIAL, False),
                       scores=self.attn_scores(lp.spatial, MOD_SPATIAL, False) if sc else None)
@@ -471,9 +482,12 @@ class _Step:
             self.run_site(li, CR, "t", self.cross_site(lp.cross_temporal, 1),
                           scores=self.cross_scores(lp.cross_temporal, 1) if sc else None)
         self.run_site(li, ML, "t", self.mlp_site(lp.mlp_temporal, MOD_MLP_T))
-        if x_in is not None and d.should_store_delta(li):
+        if x_in is not None:
             self.flush()
-            self.cache.store((li, None, "delta"), (self.r - x_in).to(torch.bfloat16), self.step, "delta")
+            delta = torch.empty_like(self.r)
+            kernels.add_scaled_(delta, self.r, x_in, -1.0)  # fp32 x - x_layer_in (model.py:565-566)
+            self.ctx.launches.other_calls += 1
+            self.cache.store((li, None, "delta"), delta, self.step, "delta")
 
 
 def run_forward(ctx: StepContext, step_index: int, t: float, z, r, decisions, cache, trace=None, flop_sink=None,

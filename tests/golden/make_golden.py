@@ -15,6 +15,10 @@ Outputs (small, committed):
                     the per-site decision log
   c1_run.npz        C1 (tiny Latte-style) latte-pab235 10-step run: per-step
                     latent norms + a strided 4096-element subsample per step
+  traces.npz        full-depth per-site decision traces (TraceRecord decision /
+                    source_step) of C2/C3/C4/C5 runs with their presets: L=28 and
+                    the configs' step counts, CFG; decisions do not depend on the
+                    hidden size, so the model is shrunk to D=8 (python run time)
 """
 
 from __future__ import annotations
@@ -202,8 +206,33 @@ def c1_run():
                         final_digest=np.array(rm.array_digest(lat[-1][None] if lat[-1].ndim == 3 else lat[-1])))
 
 
+# name: (layers, steps, preset, cross_in_temporal)
+TRACE_CONFIGS = {
+    "C2": (28, 50, "latte-pab235", False),
+    "C3": (28, 30, "opensora-pab246", True),
+    "C4": (28, 150, "opensoraplan-pab246", False),
+    "C5": (28, 30, "opensora-pab246", True),
+}
+
+
+def traces():
+    out = {}
+    for cname, (layers, steps, preset, cross_t) in TRACE_CONFIGS.items():
+        cfg = rm.ModelConfig(layers=layers, hidden=8, heads=1, frames=2, spatial_tokens=2, text_tokens=3,
+                             cross_in_temporal=cross_t)
+        params = rm.init_model(cfg, seed=11)
+        sched = rd.make_schedule(steps)
+        pol, _ = rp.resolve_preset(preset, layers)
+        for name, p in (("pab", pol), ("none", rp.NonePolicy())):
+            table = rp.build_schedule(p, sched, layers)
+            _, log = _loop(params, sched, table, seed=11, guidance=True)
+            out[f"{cname}|{name}|log"] = log
+            out[f"{cname}|{name}|table"] = table.source
+    np.savez_compressed(os.path.join(OUT, "traces.npz"), **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["decisions", "prng", "small", "c1", "scores"]
+    which = sys.argv[1:] or ["decisions", "prng", "small", "c1", "scores", "traces"]
     if "decisions" in which:
         decisions()
     if "prng" in which:
@@ -214,4 +243,6 @@ if __name__ == "__main__":
         c1_run()
     if "scores" in which:
         scores_runs()
+    if "traces" in which:
+        traces()
     print("golden fixtures written to", OUT)

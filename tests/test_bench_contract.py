@@ -27,7 +27,10 @@ def test_reference_arm_line():
     for k in BASE_KEYS:
         assert k in d, k
     assert d["impl"] == "reference" and d["higher_is_better"] is False and d["value"] > 0
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    base = d["cpu_baseline"]
+    assert base["kind"] in ("reference", "port") and base["cores"] >= 1
+    # the reference (oracle/_ref, installed by oracle/make_ref.sh) runs C1 end to end
+    assert base["extrapolated"] is (base["kind"] == "port") and d["extrapolated"] is base["extrapolated"]
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
 
 

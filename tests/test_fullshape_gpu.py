@@ -1,7 +1,7 @@
-"""Full-size parity slices: one layer of the C3 (Open-Sora
-2s 480p) block at its real shapes -- D1152, H16, T16, S1560, M300, cross in
-the temporal block, CFG batch 2 -- for 3 denoising steps whose table forces
-every kind to be broadcast at step 2, against the CPU oracle; and C5's
+"""Full-size parity slices: one layer of the C2/C3/C4 blocks at
+their real shapes (D1152, H16, T16, S1024/1560, M120/300, CFG batch 2) for a few
+denoising steps whose tables broadcast sites, against the CPU oracle; a 4-layer
+x 30-step C3 run against an oracle fixture (tests/golden/c3_deep.npz); and C5's
 3600-token spatial attention at op level against a torch fp32 reference."""
 
 import numpy as np
@@ -15,6 +15,7 @@ from paper_2408_12588_b200 import kernels  # noqa: E402
 from paper_2408_12588_b200.diffusion import Denoiser, initial_latent, make_schedule  # noqa: E402
 from paper_2408_12588_b200.model import ModelConfig, init_model  # noqa: E402
 from paper_2408_12588_b200.policies import DecisionTable  # noqa: E402
+from gates import MAX_TOL_CFG, REL_TOL_CFG  # noqa: E402
 
 
 def test_c3_layer_three_steps_with_broadcast_vs_oracle():
@@ -39,7 +40,7 @@ def test_c3_layer_three_steps_with_broadcast_vs_oracle():
     for i, (g, w) in enumerate(zip(got, want)):
         rel = np.linalg.norm(g.astype(np.float64) - w) / np.linalg.norm(w)
         mx = np.abs(g - w).max() / np.abs(w).max()
-        assert rel < 3.5e-2 and mx < 5e-2, (i, rel, mx)  # CFG (g=4) tolerance
+        assert rel < REL_TOL_CFG and mx < MAX_TOL_CFG, (i, rel, mx)  # CFG (g=4) gate, tests/gates.py
     # broadcast step is exact replay: step 2's update used the cached outputs of step 1
     assert np.isfinite(got[-1]).all()
 
@@ -71,7 +72,34 @@ def test_c2_latte_layer_pab_steps_vs_oracle():
     for i, (g, w) in enumerate(zip(got, want)):
         rel = np.linalg.norm(g.astype(np.float64) - w) / np.linalg.norm(w)
         mx = np.abs(g - w).max() / np.abs(w).max()
-        assert rel < 3.5e-2 and mx < 5e-2, (i, rel, mx)  # CFG (g=4) tolerance
+        assert rel < REL_TOL_CFG and mx < MAX_TOL_CFG, (i, rel, mx)  # CFG (g=4) gate, tests/gates.py
+
+
+def test_c4_layer_three_steps_with_broadcast_vs_oracle():
+    """C4 (Open-Sora-Plan 65f 512^2) at full shape for one layer: D1152, H16, T16,
+    S1024, M300 (T5 text), NO cross attention in the temporal block, CFG batch 2;
+    3 steps, step 2 broadcasts every site computed at step 1."""
+    cfg = ModelConfig(layers=1, hidden=1152, heads=16, frames=16, spatial_tokens=1024, text_tokens=300,
+                      cross_in_temporal=False)
+    params = init_model(cfg, seed=11)
+    src = np.zeros((3, 1, 4), dtype=np.int32)
+    src[1] = 1
+    src[2] = 1
+    table = DecisionTable(src)
+    ids = np.arange(300) % 256
+    den = Denoiser(params, make_schedule(3), table, ids, guidance=True, guidance_scale=4.0)
+    z = torch.from_numpy(initial_latent(params, 11, 2)).cuda()
+    got = []
+    den.run(z, on_step=lambda i, zz: got.append(zz.cpu().numpy().copy()))
+    assert den.ctx.launches.sites_reused == 5  # S, C, M | T, M at step 2
+    ocfg = orc.Cfg(1, 1152, 16, 16, 1024, 300, cross_in_temporal=False)
+    want = []
+    orc.sample(ocfg, orc.init_weights(ocfg, 11), orc.linear_timesteps(3), src, seed=11, text_ids=ids,
+               guidance=True, per_step=want)
+    for i, (g, w) in enumerate(zip(got, want)):
+        rel = np.linalg.norm(g.astype(np.float64) - w) / np.linalg.norm(w)
+        mx = np.abs(g - w).max() / np.abs(w).max()
+        assert rel < REL_TOL_CFG and mx < MAX_TOL_CFG, (i, rel, mx)
 
 
 def test_c5_spatial_attention_3600_tokens():

@@ -26,13 +26,8 @@ from paper_2408_12588_b200.policies import (  # noqa: E402
     resolve_preset,
 )
 
-# Tolerances: bf16 operands/outputs with fp32 accumulation and an
-# fp32 residual stream.  Unguided runs sit at the emulated-bf16 floor (~5e-3
-# relL2 measured on B200).  With classifier-free guidance the per-step update
-# uses eps_u + g (eps_c - eps_u) with g = 4, which amplifies the eps rounding
-# noise; measured floor ~1.7e-2 -> guided gate 3.5e-2 / max 5%.
-REL_TOL, MAX_TOL = 1.5e-2, 2e-2
-REL_TOL_CFG, MAX_TOL_CFG = 3.5e-2, 5e-2
+# Tolerances: tests/gates.py (guided gate = 1.5x the emulated-bf16 floor)
+from gates import MAX_TOL, MAX_TOL_CFG, REL_TOL, REL_TOL_CFG  # noqa: E402
 if os.environ.get("PAB_TEST_REPORT"):
     REL_TOL = MAX_TOL = REL_TOL_CFG = MAX_TOL_CFG = 1.0
 KIND_NAMES = [k.value for k in KINDS]

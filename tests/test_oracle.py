@@ -107,3 +107,28 @@ def test_oracle_scores_mode_matches_reference_runs(scores_runs, case, policy, gu
     for i, (got, want) in enumerate(zip(steps, data[key + "|latents"])):
         rel = np.linalg.norm(got - want) / np.linalg.norm(want)
         assert rel < 2e-5, (key, i, rel)
+
+
+# ------------------------------------------------------------ bf16 emulation
+def test_bf16_round_matches_torch():
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(5)
+    a = np.concatenate([rng.standard_normal(10000).astype(np.float32) * 10,
+                        np.array([0.0, -0.0, 1.0, 1.00390625, 1.01171875, 3.4e38, 1e-40], np.float32)])
+    want = torch.from_numpy(a).to(torch.bfloat16).float().numpy()
+    assert np.array_equal(orc.bf16_round(a), want)
+
+
+def test_emulated_bf16_floor_smoke_config():
+    """The guided gate (tests/test_model_gpu.py REL_TOL_CFG) is 1.5x the emulated
+    floor measured by scripts/bf16_floor.py; the floor of the
+    smoke config must stay where the gate was derived from (1.57e-2 relL2)."""
+    cfg = orc.Cfg(2, 144, 2, 8, 256, 20, cross_in_temporal=True)
+    w = orc.init_weights(cfg, 11)
+    ts = orc.linear_timesteps(5)
+    table = orc.table_pab(ts, 2, (2, 3, 4), (990.0, 10.0))
+    ref, emu = [], []
+    orc.sample(cfg, w, ts, table, seed=11, text_ids=np.arange(20), guidance=True, per_step=ref)
+    orc.sample(cfg, w, ts, table, seed=11, text_ids=np.arange(20), guidance=True, per_step=emu, emulate_bf16=True)
+    rel = max(np.linalg.norm(a.astype(np.float64) - b) / np.linalg.norm(b) for a, b in zip(emu, ref))
+    assert 1.0e-2 < rel < 2.0e-2, rel

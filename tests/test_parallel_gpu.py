@@ -96,3 +96,46 @@ def test_broadcast_sp_matches_serial(world, guidance, split):
     assert r0["rel"] < 2e-3, r0
     assert r0["events"] == r0["events_want"] and r0["steps_ok"] and r0["ledger_ok"], r0
     assert r0["n_cache"] > 0 and r0["cache_rel"] < 2e-3, r0
+
+
+@pytest.mark.parametrize("world,guidance,split", [(2, False, False), (4, True, False), (8, True, False),
+                                                  (4, True, True)])
+def test_logical_workers_without_process_group(world, guidance, split):
+    """run_parallel(workers=W) with no torch.distributed group runs W logical workers
+    in this process (as the reference does, parallel.py:372-464, tests/test_parallel.py:
+    111-187): threads on cuda:0 exchanging shards through LocalGroup.  Checked
+    against the CPU oracle's serial latents (gates.py) and the serial GPU engine;
+    ledger event count == 2 * L * |temporal computes| (per rank group)."""
+    from gates import MAX_TOL, MAX_TOL_CFG, REL_TOL, REL_TOL_CFG
+    from oracle import pab_oracle as orc
+    from paper_2408_12588_b200.diffusion import make_schedule, sample
+    from paper_2408_12588_b200.model import ComponentKind, ModelConfig, init_model
+    from paper_2408_12588_b200.parallel import comm_volume_model, run_parallel
+    from paper_2408_12588_b200.policies import PabPolicy, build_schedule
+
+    assert not (dist.is_available() and dist.is_initialized())
+    cfg = ModelConfig(layers=2, hidden=144, heads=2, frames=8, spatial_tokens=64, text_tokens=12,
+                      cross_in_temporal=True)
+    params = init_model(cfg, seed=3)
+    sched = make_schedule(8)
+    pol = PabPolicy(2, 3, 2, window=(990.0, 10.0))
+    table = build_schedule(pol, sched, cfg.layers)
+    par = run_parallel(params, sched, pol, world, "broadcast_sp", seed=7, guidance=guidance, table=table,
+                       split_batch=split)
+    ser = sample(params, sched, pol, seed=7, guidance=guidance, table=table)
+    rel_ser = np.linalg.norm(par.latent.astype(np.float64) - ser.latent) / np.linalg.norm(ser.latent)
+    assert rel_ser < 2e-3, rel_ser
+    ocfg = orc.Cfg(2, 144, 2, 8, 64, 12, cross_in_temporal=True)
+    want = orc.sample(ocfg, orc.init_weights(ocfg, 3), orc.linear_timesteps(8), table.source, seed=7,
+                      text_ids=np.arange(12), guidance=guidance)
+    rel = np.linalg.norm(par.latent.astype(np.float64) - want) / np.linalg.norm(want)
+    mx = np.abs(par.latent - want).max() / np.abs(want).max()
+    rt, mt = (REL_TOL_CFG, MAX_TOL_CFG) if guidance else (REL_TOL, MAX_TOL)
+    assert rel <= rt and mx <= mt, (rel, mx)
+    groups = 2 if split else 1
+    comp = table.compute_steps(ComponentKind.TEMPORAL)
+    assert par.comm_report.event_count() == 2 * cfg.layers * len(comp) * groups
+    model = comm_volume_model("broadcast_sp", cfg, sched, table, world, batch=2 if guidance else 1,
+                              split_batch=split)
+    assert par.comm_report.grouped_elements() == model.grouped_elements()
+    assert len(par.worker_caches) == world and len(par.gathered_cache()) > 0
