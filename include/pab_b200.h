@@ -169,6 +169,23 @@ int pab_attention(const pab_attn_args* args, int impl, void* stream);
  * (1 = tcgen05, 2 = SIMT).  Pure host logic, no GPU needed. */
 int pab_attention_select(const pab_attn_args* args);
 
+/*
+ * Projection GEMM on the tcgen05 tensor cores (2-CTA, TMA, TMEM accumulators).
+ * Replaces: numerics.matmul (pkg/src/pab_engine/numerics.py:72-104) for every
+ * projection of a computed site: q/k/v and o of the spatial/temporal sites
+ * (model.py:346-359), q and o of the cross sites (model.py:376-385), and the MLP
+ * w1 -> gelu -> w2 pair (model.py:398-403, gelu numerics.py:154-158).
+ *
+ *   C[m, n] = epi( sum_k A[m, k] * B[n, k] )    bf16 in/out, fp32 accumulation
+ *   A: (M, K) row stride lda; B: the weight W (K, N) stored transposed, (N, K) row
+ *   stride ldb; C: (M, N) row stride ldc (elements).
+ *   epilogue 0: bf16(acc); 1: bf16(gelu_tanh(acc)).
+ * Bases 16-byte aligned, lda/ldb/ldc/K multiples of 8; M, N, K tails are handled
+ * (zero-filled loads, clipped stores).
+ */
+int pab_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                  int64_t M, int64_t N, int64_t K, int epilogue, void* stream);
+
 /* Debug only: record a clock64 event timeline of CTA (0,0,0) of subsequent
  * tcgen05 attention launches into device_buffer (NULL disables). */
 int pab_attn_debug_trace(long long* device_buffer);

@@ -1,0 +1,364 @@
+// Projection GEMMs of the PAB sites on the 5th-gen tensor cores (sm_100a).
+//
+// reference op: numerics.matmul (pkg/src/pab_engine/numerics.py:72-104) as called for
+// every projection of a computed site -- q/k/v and o of the spatial / temporal sites
+// (model.py:346-359), q and o of the cross sites (model.py:376-385) and the two MLP
+// matrices with the tanh-GELU between them (model.py:398-403, numerics.py:154-158).
+//
+//   C[M, N] = epilogue( A[M, K] @ W[K, N] )     A, C bf16 row-major; W stored as B = W^T,
+//                                               (N, K) K-major; fp32 accumulation in TMEM
+//   epilogue 0: bf16(acc)          epilogue 1: bf16(gelu_tanh(acc))
+//
+// Design (one persistent CTA pair per TPC, 74 pairs on 148 SMs):
+//  * 2-CTA MMA (tcgen05.mma.cta_group::2): a pair computes a 256 x BN output tile; each
+//    CTA stages its own 128 rows of A and BN/2 rows of B per 64-wide K slab (TMA, 128-byte
+//    swizzle), so each SM reads half the B bytes it would need alone;
+//  * warp roles per CTA: warps 0-3 epilogue (one TMEM lane = one output row per thread),
+//    warp 4 TMA producer, warp 5 TMEM owner + MMA issuer (leader CTA only);
+//  * a 6-stage smem ring (full barriers in the leader, signalled by both CTAs' TMA
+//    transactions; empty barriers in both, released by the leader's MMA commit multicast);
+//  * two TMEM accumulators (2 x BN fp32 columns): the epilogue of tile i drains one while
+//    the MMAs of tile i+1 fill the other;
+//  * epilogue: tcgen05.ld 32 columns at a time -> (GELU) -> bf16 -> 128-byte swizzled smem
+//    staging (two 16 KB buffers) -> one TMA tensor store per 128 x 64 box.
+#include "tc_ptx.cuh"
+
+namespace pab {
+namespace gemm {
+
+using namespace pab::tc;
+
+constexpr int kBK = 64;                 // K slab per stage (one 128-byte swizzle atom of bf16)
+constexpr int kRowsCta = 128;           // A rows per CTA (pair tile M = 256)
+constexpr int kThreads = 192;           // 4 epilogue warps + producer + MMA
+constexpr int kEpiWarps = 4;
+constexpr int kProducerWarp = 4, kMmaWarp = 5;
+constexpr int kStageBoxBytes = kRowsCta * 128;  // 128 rows x 64 bf16 epilogue box
+
+template <int BN>
+struct Cfg {
+    static constexpr int kABytes = kRowsCta * kBK * 2;          // 16 KB
+    static constexpr int kBBytes = (BN / 2) * kBK * 2;          // BN/2 rows of B
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStages = (232448 - 2 * kStageBoxBytes - 1280) / kStageBytes > 8
+                                       ? 8 : (232448 - 2 * kStageBoxBytes - 1280) / kStageBytes;
+    static constexpr int kRing = kStages * kStageBytes;
+    static constexpr int kEpi0 = kRing;                          // 2 epilogue staging boxes
+    static constexpr int kBar0 = kEpi0 + 2 * kStageBoxBytes;
+    static constexpr int kSmem = kBar0 + 256 + 1024;             // barriers + 1 KB alignment slack
+    static_assert(BN % 32 == 0 && BN <= 256 && (BN / 2) % 16 == 0, "tile N");
+    static_assert(kABytes % 1024 == 0 && kBBytes % 1024 == 0, "swizzle atoms");
+    static_assert(kSmem <= 232448, "smem");
+};
+
+struct Bars {
+    uint64_t full[8], empty[8], tfull[2], tempty[2];
+};
+
+struct Params {
+    int m_tiles, n_tiles, k_slabs, tiles;
+    int epilogue;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same smem offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// 2-CTA TMA load: data lands in this CTA's smem, the transaction bytes are counted on the
+// leader CTA's barrier (peer bit of the barrier address cleared)
+__device__ __forceinline__ void tma_load_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    const uint32_t b = smem_u32(bar) & 0xFEFFFFFFu;
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(b), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void mma2(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void commit2(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+    // numerics.py:154-158: 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3)));
+    // tanh(u) = 1 - 2 / (exp(2u) + 1) (same form as the standalone GELU kernel)
+    const float u = 0.7978845608028654f * fmaf(0.044715f * x, x * x, x);
+    const float t = 1.0f - __fdividef(2.0f, __expf(2.0f * u) + 1.0f);
+    return 0.5f * x * (1.0f + t);
+}
+
+// tile t -> (m, n): groups of 8 M-tiles sweep all N tiles, so the pairs in flight share
+// A row blocks and the (small) weight matrix stays L2-resident
+__device__ __forceinline__ void tile_coords(int t, const Params& p, int& m, int& n) {
+    constexpr int G = 8;
+    const int per_group = G * p.n_tiles;
+    const int g = t / per_group, r = t - g * per_group;
+    const int gm = min(G, p.m_tiles - g * G);
+    m = g * G + r % gm;
+    n = r / gm;
+}
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                const __grid_constant__ CUtensorMap map_c, const Params p) {
+    using C = Cfg<BN>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    Bars* bars = reinterpret_cast<Bars*>(smem + C::kBar0);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kBar0 + sizeof(Bars));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(&bars->full[s], 1);
+            mbar_init(&bars->empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&bars->tfull[a], 1);
+            mbar_init(&bars->tempty[a], 2 * kEpiWarps);  // both CTAs' epilogue warps
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == kProducerWarp && lane == 0) {
+        prefetch_map(&map_a);
+        prefetch_map(&map_b);
+        prefetch_map(&map_c);
+    }
+    if (warp == kMmaWarp) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == kProducerWarp) {
+        // ================================================================ TMA producer
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = pair; t < p.tiles; t += n_pairs) {
+                int tm, tn;
+                tile_coords(t, p, tm, tn);
+                const int row = tm * 2 * kRowsCta + (int)rank * kRowsCta;
+                const int col = tn * BN + (int)rank * (BN / 2);
+                for (int kb = 0; kb < p.k_slabs; ++kb) {
+                    mbar_wait(&bars->empty[s], ph ^ 1);
+                    if (leader) mbar_expect_tx(&bars->full[s], 2 * C::kStageBytes);
+                    uint8_t* st = smem + s * C::kStageBytes;
+                    tma_load_2sm(st, &map_a, &bars->full[s], kb * kBK, row);
+                    tma_load_2sm(st + C::kABytes, &map_b, &bars->full[s], kb * kBK, col);
+                    if (++s == C::kStages) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        // ================================================================ MMA issuer (leader)
+        if (leader) {
+            constexpr uint32_t idesc = idesc_bf16(256, BN, 0);
+            constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (kLayoutSW128 << 29);
+            constexpr uint32_t kLbo = (16u >> 4) << 16;
+            const uint32_t base_lo = smem_u32(smem) >> 4;
+            int s = 0, acc = 0;
+            uint32_t ph = 0, aph = 0;
+            for (int t = pair; t < p.tiles; t += n_pairs) {
+                mbar_wait(&bars->tempty[acc], aph ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(acc * BN);
+                for (int kb = 0; kb < p.k_slabs; ++kb) {
+                    mbar_wait(&bars->full[s], ph);
+                    tc_fence_after();
+                    const uint32_t a_lo = base_lo + ((s * C::kStageBytes) >> 4);
+                    const uint32_t b_lo = a_lo + (C::kABytes >> 4);
+                    if (lane == 0) {
+#pragma unroll
+                        for (int k = 0; k < kBK / 16; ++k) {
+                            const uint64_t da = ((uint64_t)kHi << 32) | ((a_lo + 2 * k) | kLbo);
+                            const uint64_t db = ((uint64_t)kHi << 32) | ((b_lo + 2 * k) | kLbo);
+                            mma2(d, da, db, idesc, (kb | k) != 0);
+                        }
+                        commit2(&bars->empty[s]);
+                    }
+                    __syncwarp();
+                    if (++s == C::kStages) { s = 0; ph ^= 1; }
+                }
+                if (lane == 0) commit2(&bars->tfull[acc]);
+                __syncwarp();
+                if (++acc == 2) { acc = 0; aph ^= 1; }
+            }
+        }
+    } else {
+        // ================================================================ epilogue (warps 0-3)
+        const int r = threadIdx.x;  // row within the CTA's 128-row half == TMEM lane
+        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+        const uint32_t tempty_leader0 = mapa(smem_u32(&bars->tempty[0]), 0);
+        const uint32_t tempty_leader1 = mapa(smem_u32(&bars->tempty[1]), 0);
+        uint8_t* stage0 = smem + C::kEpi0;
+        int acc = 0, box = 0;
+        uint32_t aph = 0;
+        for (int t = pair; t < p.tiles; t += n_pairs) {
+            int tm, tn;
+            tile_coords(t, p, tm, tn);
+            const int row0 = tm * 2 * kRowsCta + (int)rank * kRowsCta;
+            mbar_wait(&bars->tfull[acc], aph);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < BN / 64; ++c) {
+                float v[64];
+                const uint32_t ta = tmem + lane_base + (uint32_t)(acc * BN + c * 64);
+                PAB_TMEM_LD32(ta, v);
+                PAB_TMEM_LD32(ta + 32, (v + 32));
+                tmem_wait_ld();
+                if (c == BN / 64 - 1) {
+                    // accumulator fully in registers: hand it back to the MMA warp
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+                }
+                if (p.epilogue == 1) {
+#pragma unroll
+                    for (int i = 0; i < 64; ++i) v[i] = gelu_tanh(v[i]);
+                }
+                uint8_t* sb = stage0 + box * kStageBoxBytes;
+                // the TMA store issued from this buffer two boxes ago must have read it
+                if (threadIdx.x == 0) bulk_wait_read<1>();
+                named_bar(1, 128);
+                const uint32_t rowaddr = smem_u32(sb) + (uint32_t)r * 128;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t a = rowaddr + (uint32_t)(((j ^ (r & 7)) * 16));
+                    st_shared_v4(a, pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                                 pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+                }
+                fence_async_smem();
+                named_bar(1, 128);
+                if (threadIdx.x == 0) {
+                    tma_store_2d(&map_c, sb, tn * BN + c * 64, row0);
+                    bulk_commit();
+                }
+                box ^= 1;
+            }
+            if (++acc == 2) { acc = 0; aph ^= 1; }
+        }
+        if (threadIdx.x == 0) bulk_wait_all();
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == kMmaWarp) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
+static bool map_2d(CUtensorMap* m, const void* base, int64_t inner, int64_t outer, int64_t ld_elems, int box_inner,
+                   int box_outer) {
+    auto encode = get_encode();
+    if (!encode) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+    cuuint64_t strides[1] = {(cuuint64_t)ld_elems * 2};
+    cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int g_sms = 0;
+
+template <int BN>
+static int launch(const void* A, int64_t lda, const void* B, int64_t ldb, void* Cp, int64_t ldc, int64_t M,
+                  int64_t N, int64_t K, int epilogue, cudaStream_t st) {
+    using C = Cfg<BN>;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
+            cudaSuccess)
+            return launch_status("gemm smem attribute");
+        attr = true;
+    }
+    CUtensorMap ma, mb, mc;
+    if (!map_2d(&ma, A, K, M, lda, kBK, kRowsCta) || !map_2d(&mb, B, K, N, ldb, kBK, BN / 2) ||
+        !map_2d(&mc, Cp, N, M, ldc, 64, kRowsCta))
+        return PAB_ERR_CUDA;
+    Params p;
+    p.m_tiles = (int)((M + 2 * kRowsCta - 1) / (2 * kRowsCta));
+    p.n_tiles = (int)((N + BN - 1) / BN);  // a partial last N tile: B rows zero-filled, C columns clipped
+    p.k_slabs = (int)((K + kBK - 1) / kBK);
+    p.tiles = p.m_tiles * p.n_tiles;
+    p.epilogue = epilogue;
+    if (g_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int pairs = g_sms / 2;
+    if (pairs > p.tiles) pairs = p.tiles;
+    gemm_kernel<BN><<<2 * pairs, kThreads, C::kSmem, st>>>(ma, mb, mc, p);
+    return launch_status("gemm");
+}
+
+}  // namespace gemm
+}  // namespace pab
+
+extern "C" int pab_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                             int64_t M, int64_t N, int64_t K, int epilogue, void* stream) {
+    using namespace pab::gemm;
+    if (M < 0 || N <= 0 || K <= 0) return M == 0 ? PAB_OK : PAB_ERR_SHAPE;
+    if (M == 0) return PAB_OK;
+    if (!A || !B || !C) return PAB_ERR_INVALID;
+    if (epilogue != 0 && epilogue != 1) return PAB_ERR_INVALID;
+    if (lda < K || ldb < K || ldc < N) return PAB_ERR_SHAPE;
+    // TMA: 16-byte aligned bases and row strides (M, N and K tails are zero-filled / clipped)
+    if ((uintptr_t)A % 16 || (uintptr_t)B % 16 || (uintptr_t)C % 16 || lda % 8 || ldb % 8 || ldc % 8 || K % 8)
+        return PAB_ERR_UNSUPPORTED;
+    if (M > 0x7fffffff || N > 0x7fffffff || K > 0x7fffffff) return PAB_ERR_UNSUPPORTED;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (N % 256 == 0 && N >= 4096) return launch<256>(A, lda, B, ldb, C, ldc, M, N, K, epilogue, st);
+    if (N % 192 == 0) return launch<192>(A, lda, B, ldb, C, ldc, M, N, K, epilogue, st);
+    return launch<128>(A, lda, B, ldb, C, ldc, M, N, K, epilogue, st);
+}

@@ -186,6 +186,26 @@ def fill_uniform(dst: torch.Tensor, rows: int, cols: int, col0: int, state: int,
     )
 
 
+EPI_NONE, EPI_GELU = 0, 1
+
+
+def gemm(a: torch.Tensor, w_t: torch.Tensor, out: torch.Tensor, epilogue: int = EPI_NONE) -> torch.Tensor:
+    """out = epi(a @ w_t^T) on the tcgen05 GEMM: a (M, K), w_t (N, K) (the weight stored
+    transposed, K-major), out (M, N); bf16, unit column stride, any row strides."""
+    lib = _lib.load()
+    for t, name in ((a, "A"), (w_t, "B"), (out, "C")):
+        _need(t, torch.bfloat16, name)
+        if t.dim() != 2 or t.stride(1) != 1:
+            raise ShapeError(f"gemm operand {name} must be 2-D with unit column stride")
+    M, K = a.shape
+    N = w_t.shape[0]
+    if w_t.shape[1] != K or out.shape != (M, N):
+        raise ShapeError(f"gemm shapes {tuple(a.shape)} x {tuple(w_t.shape)}^T -> {tuple(out.shape)}")
+    _lib.check(lib.pab_gemm_bf16(a.data_ptr(), a.stride(0), w_t.data_ptr(), w_t.stride(0), out.data_ptr(),
+                                 out.stride(0), M, N, K, int(epilogue), _stream()), "pab_gemm_bf16")
+    return out
+
+
 def attn_args(q, k, v, o, qs, ks, vs, os_, n_a, n_b, n_q, n_k, heads, dh, scale=None) -> _lib.AttnArgs:
     """Build pab_attn_args; *s are (s_a, s_b, s_i) element strides of each operand."""
     for t, name in ((q, "q"), (k, "k"), (v, "v"), (o, "o")):

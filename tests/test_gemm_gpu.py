@@ -1,0 +1,59 @@
+"""The tcgen05 projection GEMM (pab_gemm_bf16, csrc/gemm.cu) against a torch fp32
+reference of the same bf16 operands: every C2-C5 projection shape, GELU epilogue,
+M/N/K tails and strided operands (the cross sites' live-row views)."""
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2408_12588_b200 import kernels  # noqa: E402
+
+
+def _ref(a, w_t, epilogue):
+    y = a.float() @ w_t.float().t()
+    if epilogue == kernels.EPI_GELU:
+        y = 0.5 * y * (1.0 + torch.tanh(0.7978845608028654 * (y + 0.044715 * y ** 3)))
+    return y
+
+
+def _check(M, N, K, epilogue=0, lda=None, ldc=None, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    lda, ldc = lda or K, ldc or N
+    abuf = torch.randn(M, lda, device="cuda", generator=g).to(torch.bfloat16)
+    a = abuf[:, :K]
+    w_t = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    cbuf = torch.full((M, ldc), 7.0, device="cuda", dtype=torch.bfloat16)
+    c = cbuf[:, :N]
+    kernels.gemm(a, w_t, c, epilogue)
+    ref = _ref(a, w_t, epilogue)
+    err = (c.float() - ref).abs().max().item()
+    scale = ref.abs().max().item()
+    # bf16 output rounding (2^-9 relative) + fp32 accumulation-order differences
+    assert err <= 8e-3 * scale + 1e-3, (M, N, K, epilogue, err, scale)
+    if ldc > N:
+        assert torch.all(cbuf[:, N:] == 7.0), "GEMM wrote past N"
+    return err / scale
+
+
+@pytest.mark.parametrize("M,N,K", [(49920, 3456, 1152), (49920, 1152, 1152), (49920, 1152, 4608),
+                                   (32768, 2304, 1152), (24960, 1152, 1152), (600, 2304, 1152)])
+def test_gemm_projection_shapes(M, N, K):
+    _check(M, N, K)
+
+
+def test_gemm_gelu_epilogue_w1_shape():
+    _check(49920, 4608, 1152, kernels.EPI_GELU)
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 8, 8), (100, 144, 144), (257, 432, 144), (300, 96, 48), (513, 32, 32),
+                                   (2048, 576, 144), (130, 1152, 4608), (4096, 4608, 1152)])
+def test_gemm_tails(M, N, K):
+    _check(M, N, K)
+    _check(M, N, K, kernels.EPI_GELU)
+
+
+def test_gemm_strided_operands():
+    # A / C as column slices of wider rows (the fused [q|k|v] buffer, live-row views)
+    _check(3000, 1152, 1152, lda=3456, ldc=3456)
+    _check(777, 384, 1152, lda=1160, ldc=400)
