@@ -148,10 +148,11 @@ int pab_fill_uniform(void* dst, int dtype, int64_t rows, int64_t cols, int64_t l
  *   temporal: a = batch, b = token, i = frame        (rows of (B,T,S,D))
  *   cross   : a = batch, i = (frame, token) for q/o, i = text token for k/v
  * Output o uses the same addressing with (o_sa, o_sb, o_si).
- * impl: 0 = auto (tcgen05/TMA kernel when the shape allows), 1 = force the
- * tcgen05 kernels (row-per-thread kernel for long sequences, block-diagonal
- * packed kernel for short ones; error if unsupported), 2 = force the SIMT
- * kernel, 3 = the earlier split-row tcgen05 kernel for every shape (A/B only).
+ * impl: 0 or 1 = the tcgen05/TMA kernels (row-per-thread kernel for long
+ * sequences, block-diagonal packed kernel for short ones); shapes they cannot
+ * address (dh not a multiple of 8 or > 80, unaligned strides) return
+ * PAB_ERR_UNSUPPORTED -- there is no silent fallback.  2 = the SIMT kernel,
+ * a test cross-check only (any dh <= 128).
  */
 typedef struct {
     const void* q; const void* k; const void* v; void* o;
@@ -165,8 +166,8 @@ typedef struct {
 
 int pab_attention(const pab_attn_args* args, int impl, void* stream);
 
-/* Which attention implementation `impl=0` would select for these args
- * (1 = tcgen05, 2 = SIMT).  Pure host logic, no GPU needed. */
+/* 1 if the tcgen05 kernels support these args (what impl=0 runs), else 0.
+ * Pure host logic, no GPU needed. */
 int pab_attention_select(const pab_attn_args* args);
 
 /*

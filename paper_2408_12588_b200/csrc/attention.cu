@@ -113,23 +113,21 @@ using namespace pab;
 
 extern "C" int pab_attention_select(const pab_attn_args* a) {
     if (!args_valid(a)) return 0;
-    return attn_tc_supported(a) ? 1 : 2;
+    return attn_tc_supported(a) ? 1 : 0;
 }
 
 extern "C" int pab_attention(const pab_attn_args* a, int impl, void* stream) {
     if (!args_valid(a)) return PAB_ERR_SHAPE;
     if (a->n_a == 0 || a->n_b == 0 || a->n_q == 0) return PAB_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    if (impl == 0) impl = attn_tc_supported(a) ? 1 : 2;
+    // one product path: the tcgen05 kernels; shapes they cannot address are an error, not
+    // a silent fallback (the SIMT kernel runs only when asked for by name, as a cross-check)
+    if (impl == 0) impl = 1;
     if (impl == 1) {
         // long sequences: row-per-thread kernel (attn_fa.cu); short packed sequences
         // (temporal attention): block-diagonal kernel (attn_tc.cu)
         if (!attn_tc_supported(a)) return PAB_ERR_UNSUPPORTED;
         return (attn_tc_packing(a) || !attn_fa_supported(a)) ? attn_tc_launch(a, st) : attn_fa_launch(a, st);
-    }
-    if (impl == 3) {  // previous split-row kernel for every shape (A/B comparisons)
-        if (!attn_tc_supported(a)) return PAB_ERR_UNSUPPORTED;
-        return attn_tc_launch(a, st);
     }
     if (impl == 2) return attn_simt_launch(a, st);
     return PAB_ERR_INVALID;

@@ -30,21 +30,28 @@ using namespace pab::tc;
 
 constexpr int kBK = 64;                 // K slab per stage (one 128-byte swizzle atom of bf16)
 constexpr int kRowsCta = 128;           // A rows per CTA (pair tile M = 256)
-constexpr int kThreads = 192;           // 4 epilogue warps + producer + MMA
-constexpr int kEpiWarps = 4;
-constexpr int kProducerWarp = 4, kMmaWarp = 5;
+#ifndef PAB_GEMM_EPI_WARPS
+#define PAB_GEMM_EPI_WARPS 8  // 4: one epilogue warp per SM sub-partition; 8: two (overlap TMEM loads and math)
+#endif
+constexpr int kEpiWarps = PAB_GEMM_EPI_WARPS;
+constexpr int kEpiGroups = kEpiWarps / 4;
+constexpr int kBufPerGroup = kEpiGroups == 1 ? 2 : 1;   // epilogue staging boxes per warp group
+constexpr int kThreads = 32 * (kEpiWarps + 2);          // epilogue warps + producer + MMA
+constexpr int kProducerWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
 constexpr int kStageBoxBytes = kRowsCta * 128;  // 128 rows x 64 bf16 epilogue box
+static_assert(kEpiWarps == 4 || kEpiWarps == 8, "epilogue warps");
 
 template <int BN>
 struct Cfg {
     static constexpr int kABytes = kRowsCta * kBK * 2;          // 16 KB
     static constexpr int kBBytes = (BN / 2) * kBK * 2;          // BN/2 rows of B
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStages = (232448 - 2 * kStageBoxBytes - 1280) / kStageBytes > 8
-                                       ? 8 : (232448 - 2 * kStageBoxBytes - 1280) / kStageBytes;
+    static constexpr int kEpiBytes = kEpiGroups * kBufPerGroup * kStageBoxBytes;
+    static constexpr int kStages = (232448 - kEpiBytes - 1280) / kStageBytes > 8
+                                       ? 8 : (232448 - kEpiBytes - 1280) / kStageBytes;
     static constexpr int kRing = kStages * kStageBytes;
-    static constexpr int kEpi0 = kRing;                          // 2 epilogue staging boxes
-    static constexpr int kBar0 = kEpi0 + 2 * kStageBoxBytes;
+    static constexpr int kEpi0 = kRing;                          // epilogue staging boxes
+    static constexpr int kBar0 = kEpi0 + kEpiBytes;
     static constexpr int kSmem = kBar0 + 256 + 1024;             // barriers + 1 KB alignment slack
     static_assert(BN % 32 == 0 && BN <= 256 && (BN / 2) % 16 == 0, "tile N");
     static_assert(kABytes % 1024 == 0 && kBBytes % 1024 == 0, "swizzle atoms");
@@ -120,11 +127,11 @@ __device__ __forceinline__ void commit2(uint64_t* bar) {
 }
 
 __device__ __forceinline__ float gelu_tanh(float x) {
-    // numerics.py:154-158: 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3)));
-    // tanh(u) = 1 - 2 / (exp(2u) + 1) (same form as the standalone GELU kernel)
-    const float u = 0.7978845608028654f * fmaf(0.044715f * x, x * x, x);
-    const float t = 1.0f - __fdividef(2.0f, __expf(2.0f * u) + 1.0f);
-    return 0.5f * x * (1.0f + t);
+    // numerics.py:154-158: 0.5 x (1 + tanh(u)), u = sqrt(2/pi) (x + 0.044715 x^3),
+    // evaluated as x * sigmoid(2u) = x / (1 + exp(-2u)) (identical; no cancellation in the
+    // negative tail); exp via ex2 with the log2(e) factor folded into the constant
+    const float z = -2.0f * 1.4426950408889634f * 0.7978845608028654f * fmaf(0.044715f * x, x * x, x);
+    return __fdividef(x, 1.0f + fast_exp2(z));
 }
 
 // tile t -> (m, n): groups of 8 M-tiles sweep all N tiles, so the pairs in flight share
@@ -233,14 +240,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
     } else {
-        // ================================================================ epilogue (warps 0-3)
-        const int r = threadIdx.x;  // row within the CTA's 128-row half == TMEM lane
-        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+        // ============================================ epilogue (warps 0 .. kEpiWarps-1)
+        // kEpiGroups groups of 4 warps; group g drains 64-column chunks c = g, g + kEpiGroups,
+        // ... of each accumulator (a thread owns one TMEM lane == one output row)
+        const int g = warp >> 2;
+        const int r = threadIdx.x & 127;  // row within the CTA's 128-row half == TMEM lane
+        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
         const uint32_t tempty_leader0 = mapa(smem_u32(&bars->tempty[0]), 0);
         const uint32_t tempty_leader1 = mapa(smem_u32(&bars->tempty[1]), 0);
-        uint8_t* stage0 = smem + C::kEpi0;
+        uint8_t* stage0 = smem + C::kEpi0 + g * kBufPerGroup * kStageBoxBytes;
         int acc = 0, box = 0;
         uint32_t aph = 0;
+        constexpr int kChunks = BN / 64;
         for (int t = pair; t < p.tiles; t += n_pairs) {
             int tm, tn;
             tile_coords(t, p, tm, tn);
@@ -248,14 +259,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbar_wait(&bars->tfull[acc], aph);
             tc_fence_after();
 #pragma unroll 1
-            for (int c = 0; c < BN / 64; ++c) {
+            for (int c = g; c < kChunks; c += kEpiGroups) {
                 float v[64];
                 const uint32_t ta = tmem + lane_base + (uint32_t)(acc * BN + c * 64);
                 PAB_TMEM_LD32(ta, v);
                 PAB_TMEM_LD32(ta + 32, (v + 32));
                 tmem_wait_ld();
-                if (c == BN / 64 - 1) {
-                    // accumulator fully in registers: hand it back to the MMA warp
+                if (c + kEpiGroups >= kChunks) {
+                    // this warp's last chunk of the accumulator is in registers: release it
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
@@ -265,9 +276,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     for (int i = 0; i < 64; ++i) v[i] = gelu_tanh(v[i]);
                 }
                 uint8_t* sb = stage0 + box * kStageBoxBytes;
-                // the TMA store issued from this buffer two boxes ago must have read it
-                if (threadIdx.x == 0) bulk_wait_read<1>();
-                named_bar(1, 128);
+                // the TMA store issued from this buffer kBufPerGroup boxes ago must have read it
+                if (r == 0) bulk_wait_read<kBufPerGroup - 1>();
+                named_bar(1 + g, 128);
                 const uint32_t rowaddr = smem_u32(sb) + (uint32_t)r * 128;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
@@ -276,16 +287,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                  pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
                 }
                 fence_async_smem();
-                named_bar(1, 128);
-                if (threadIdx.x == 0) {
+                named_bar(1 + g, 128);
+                if (r == 0) {
                     tma_store_2d(&map_c, sb, tn * BN + c * 64, row0);
                     bulk_commit();
                 }
-                box ^= 1;
+                if (++box == kBufPerGroup) box = 0;
             }
             if (++acc == 2) { acc = 0; aph ^= 1; }
         }
-        if (threadIdx.x == 0) bulk_wait_all();
+        if (r == 0) bulk_wait_all();
     }
     tc_fence_before();
     cluster_sync();

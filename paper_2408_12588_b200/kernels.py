@@ -16,8 +16,8 @@ from . import _lib
 from .errors import ShapeError, ValidationError
 
 MAX_PENDING = _lib.MAX_PENDING
-# IMPL_TC_SPLIT: the earlier split-row tcgen05 kernel for every shape (A/B comparisons only)
-IMPL_AUTO, IMPL_TCGEN05, IMPL_SIMT, IMPL_TC_SPLIT = 0, 1, 2, 3
+# IMPL_SIMT: the SIMT attention kernel, a test cross-check only (never selected automatically)
+IMPL_AUTO, IMPL_TCGEN05, IMPL_SIMT = 0, 1, 2
 
 
 def _stream() -> int:

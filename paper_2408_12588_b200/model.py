@@ -127,37 +127,57 @@ class AttnParams:
     ln_gamma: object
     ln_beta: object
     w_mod: object      # fp32 (D, 2D)
-    w_qkv: object      # bf16 (D, 3D) = [wq | wk | wv]
-    wo: object         # bf16 (D, D)
+    w_qkv_t: object    # bf16 (3D, D) = [wq | wk | wv]^T: K-major GEMM operand (pab_gemm_bf16)
+    wo_t: object       # bf16 (D, D) = wo^T
+
+    @property
+    def w_qkv(self):
+        return self.w_qkv_t.t()
+
+    @property
+    def wo(self):
+        return self.wo_t.t()
 
     @property
     def wq(self):
-        return self.w_qkv[:, : self.wo.shape[0]]
+        return self.w_qkv[:, : self.wo_t.shape[0]]
 
     @property
     def wk(self):
-        d = self.wo.shape[0]
+        d = self.wo_t.shape[0]
         return self.w_qkv[:, d : 2 * d]
 
     @property
     def wv(self):
-        d = self.wo.shape[0]
+        d = self.wo_t.shape[0]
         return self.w_qkv[:, 2 * d :]
 
 
 @dataclass
 class CrossParams:
-    wq: object         # bf16 (D, D)
-    w_kv: object       # bf16 (D, 2D) = [wk | wv]
-    wo: object
+    wq_t: object       # bf16 (D, D) = wq^T
+    w_kv_t: object     # bf16 (2D, D) = [wk | wv]^T
+    wo_t: object
+
+    @property
+    def wq(self):
+        return self.wq_t.t()
+
+    @property
+    def w_kv(self):
+        return self.w_kv_t.t()
+
+    @property
+    def wo(self):
+        return self.wo_t.t()
 
     @property
     def wk(self):
-        return self.w_kv[:, : self.wq.shape[0]]
+        return self.w_kv[:, : self.wq_t.shape[0]]
 
     @property
     def wv(self):
-        return self.w_kv[:, self.wq.shape[0] :]
+        return self.w_kv[:, self.wq_t.shape[0] :]
 
 
 @dataclass
@@ -165,8 +185,16 @@ class MlpParams:
     ln_gamma: object
     ln_beta: object
     w_mod: object
-    w1: object
-    w2: object
+    w1_t: object       # bf16 (R, D) = w1^T
+    w2_t: object       # bf16 (D, R) = w2^T
+
+    @property
+    def w1(self):
+        return self.w1_t.t()
+
+    @property
+    def w2(self):
+        return self.w2_t.t()
 
 
 @dataclass
@@ -250,25 +278,14 @@ def init_model(cfg: ModelConfig, seed: int, dtype=np.float32, device="cuda") -> 
     ones = torch.ones(d, **f32)
     zeros = torch.zeros(d, **f32)
 
-    layers = []
-    for li in range(L):
-        def attn(slot):
-            return AttnParams(ones, zeros, w_mod_all[li, slot], torch.empty((d, 3 * d), **bf16),
-                              torch.empty((d, d), **bf16))
+    # GEMM weights are drawn into their reference (K, N) layout, then stored transposed
+    # ((N, K), K-major) as the tcgen05 GEMM's B operand
+    nat: dict = {}
 
-        def cross():
-            return CrossParams(torch.empty((d, d), **bf16), torch.empty((d, 2 * d), **bf16),
-                               torch.empty((d, d), **bf16))
-
-        def mlp(slot):
-            return MlpParams(ones, zeros, w_mod_all[li, slot], torch.empty((d, r), **bf16),
-                             torch.empty((r, d), **bf16))
-
-        layers.append(LayerParams(
-            spatial=attn(MOD_SPATIAL), cross_spatial=cross(), mlp_spatial=mlp(MOD_MLP_S),
-            temporal=attn(MOD_TEMPORAL), cross_temporal=cross() if cfg.cross_in_temporal else None,
-            mlp_temporal=mlp(MOD_MLP_T),
-        ))
+    def buf(key, rows, cols):
+        if key not in nat:
+            nat[key] = torch.empty((rows, cols), **bf16)
+        return nat[key]
 
     def target(name):
         """(tensor, column offset) receiving the named draw."""
@@ -277,27 +294,48 @@ def init_model(cfg: ModelConfig, seed: int, dtype=np.float32, device="cuda") -> 
         if name == "w_time":
             return w_time, 0
         _, li, site, w = name.split(".")
-        lp = layers[int(li)]
-        obj = getattr(lp, site)
-        if isinstance(obj, AttnParams):
-            if w == "w_mod":
-                return obj.w_mod, 0
+        if w == "w_mod":
+            slot = {"spatial": MOD_SPATIAL, "mlp_spatial": MOD_MLP_S, "temporal": MOD_TEMPORAL,
+                    "mlp_temporal": MOD_MLP_T}[site]
+            return w_mod_all[int(li), slot], 0
+        if site in ("spatial", "temporal"):
             if w in ("wq", "wk", "wv"):
-                return obj.w_qkv, "qkv".index(w[1]) * d
-            return obj.wo, 0
-        if isinstance(obj, CrossParams):
-            if w == "wq":
-                return obj.wq, 0
+                return buf((li, site, "qkv"), d, 3 * d), "qkv".index(w[1]) * d
+            return buf((li, site, "o"), d, d), 0
+        if site.startswith("cross"):
             if w in ("wk", "wv"):
-                return obj.w_kv, (0 if w == "wk" else d)
-            return obj.wo, 0
-        return getattr(obj, w), 0
+                return buf((li, site, "kv"), d, 2 * d), (0 if w == "wk" else d)
+            return buf((li, site, w), d, d), 0
+        return buf((li, site, w), *((d, r) if w == "w1" else (r, d))), 0
 
     offset = 0
     for name, rows, cols in param_draw_plan(cfg):
         dst, col0 = target(name)
         kernels.fill_uniform(dst, rows, cols, col0, state, offset, -bound, bound)
         offset += rows * cols
+
+    def t_(key):
+        return nat.pop(key).t().contiguous()
+
+    layers = []
+    for li in range(L):
+        k = str(li)
+
+        def attn(site, slot):
+            return AttnParams(ones, zeros, w_mod_all[li, slot], t_((k, site, "qkv")), t_((k, site, "o")))
+
+        def cross(site):
+            return CrossParams(t_((k, site, "wq")), t_((k, site, "kv")), t_((k, site, "wo")))
+
+        def mlp(site, slot):
+            return MlpParams(ones, zeros, w_mod_all[li, slot], t_((k, site, "w1")), t_((k, site, "w2")))
+
+        layers.append(LayerParams(
+            spatial=attn("spatial", MOD_SPATIAL), cross_spatial=cross("cross_spatial"),
+            mlp_spatial=mlp("mlp_spatial", MOD_MLP_S), temporal=attn("temporal", MOD_TEMPORAL),
+            cross_temporal=cross("cross_temporal") if cfg.cross_in_temporal else None,
+            mlp_temporal=mlp("mlp_temporal", MOD_MLP_T),
+        ))
     return ModelParams(cfg=cfg, seed=seed, dtype=np.dtype(np.float32), text_table=text_table, w_time=w_time,
                        layers=layers, w_mod_all=w_mod_all, ln_identity=True)
 

@@ -381,9 +381,9 @@ class _SPTemporal:
             st.src, st.pending = st.r, []
             exchange_frames_to_tokens(self.h_send, self.h_tok, self.group)
             self._log(st.step, li)
-            torch.mm(self.h_tok.view(-1, ctx.D), p.w_qkv, out=self.qkv_tok)
+            kernels.gemm(self.h_tok.view(-1, ctx.D), p.w_qkv_t, self.qkv_tok)
             kernels.attention(self.args, ctx.attn_impl)
-            torch.mm(self.attn_tok, p.wo, out=self.o_tok.view(-1, ctx.D))
+            kernels.gemm(self.attn_tok, p.wo_t, self.o_tok.view(-1, ctx.D))
             exchange_tokens_to_frames(self.o_tok, self.o_recv, self.group)
             self._log(st.step, li)
             o = st.out_buffer(store)
