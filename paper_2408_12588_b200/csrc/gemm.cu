@@ -10,9 +10,10 @@
 //   epilogue 0: bf16(acc)          epilogue 1: bf16(gelu_tanh(acc))
 //
 // Design (one persistent CTA pair per TPC, 74 pairs on 148 SMs):
-//  * 2-CTA MMA (tcgen05.mma.cta_group::2): a pair computes a 256 x BN output tile; each
-//    CTA stages its own 128 rows of A and BN/2 rows of B per 64-wide K slab (TMA, 128-byte
-//    swizzle), so each SM reads half the B bytes it would need alone;
+//  * 2-CTA MMA (tcgen05.mma.cta_group::2): a pair computes a 256 x 256 output tile; each
+//    CTA stages its own 128 rows of A and 128 rows of B per 64-wide K slab (TMA, 128-byte
+//    swizzle), so each SM reads half the B bytes it would need alone; N % 256 is covered by
+//    one narrower last tile (MMA N = the remainder rounded up to 64);
 //  * warp roles per CTA: warps 0-3 epilogue (one TMEM lane = one output row per thread),
 //    warp 4 TMA producer, warp 5 TMEM owner + MMA issuer (leader CTA only);
 //  * a 6-stage smem ring (full barriers in the leader, signalled by both CTAs' TMA
@@ -22,6 +23,7 @@
 //  * epilogue: tcgen05.ld 32 columns at a time -> (GELU) -> bf16 -> 128-byte swizzled smem
 //    staging (two 16 KB buffers) -> one TMA tensor store per 128 x 64 box.
 #include "tc_ptx.cuh"
+#include <stdlib.h>
 
 namespace pab {
 namespace gemm {
@@ -64,7 +66,9 @@ struct Bars {
 
 struct Params {
     int m_tiles, n_tiles, k_slabs, tiles;
+    int n_last;    // width of the last N tile (a multiple of 64, <= BN): N = (n_tiles-1)*BN + n_last - pad
     int epilogue;
+    int group;  // M tiles per raster group
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -137,7 +141,7 @@ __device__ __forceinline__ float gelu_tanh(float x) {
 // tile t -> (m, n): groups of 8 M-tiles sweep all N tiles, so the pairs in flight share
 // A row blocks and the (small) weight matrix stays L2-resident
 __device__ __forceinline__ void tile_coords(int t, const Params& p, int& m, int& n) {
-    constexpr int G = 8;
+    const int G = p.group;
     const int per_group = G * p.n_tiles;
     const int g = t / per_group, r = t - g * per_group;
     const int gm = min(G, p.m_tiles - g * G);
@@ -145,7 +149,7 @@ __device__ __forceinline__ void tile_coords(int t, const Params& p, int& m, int&
     n = r / gm;
 }
 
-template <int BN>
+template <int BN, bool NARROW>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 const __grid_constant__ CUtensorMap map_c, const Params p) {
@@ -193,7 +197,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 int tm, tn;
                 tile_coords(t, p, tm, tn);
                 const int row = tm * 2 * kRowsCta + (int)rank * kRowsCta;
-                const int col = tn * BN + (int)rank * (BN / 2);
+                const int width = (NARROW && tn == p.n_tiles - 1) ? p.n_last : BN;
+                const int col = tn * BN + (int)rank * (width / 2);
                 for (int kb = 0; kb < p.k_slabs; ++kb) {
                     mbar_wait(&bars->empty[s], ph ^ 1);
                     if (leader) mbar_expect_tx(&bars->full[s], 2 * C::kStageBytes);
@@ -207,16 +212,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     } else if (warp == kMmaWarp) {
         // ================================================================ MMA issuer (leader)
         if (leader) {
-            constexpr uint32_t idesc = idesc_bf16(256, BN, 0);
+            constexpr uint32_t idesc_full = idesc_bf16(256, BN, 0);
+            const uint32_t idesc_last = idesc_bf16(256, p.n_last, 0);
             constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (kLayoutSW128 << 29);
             constexpr uint32_t kLbo = (16u >> 4) << 16;
             const uint32_t base_lo = smem_u32(smem) >> 4;
             int s = 0, acc = 0;
             uint32_t ph = 0, aph = 0;
+            // NARROW: the last N tile is narrower -- its MMAs have N = n_last (each CTA supplies
+            // n_last / 2 rows of B), so a 3456-wide output is 13 x 256 + 128, not 14 x 256.
+            // A separate instantiation: the per-tile (m, n) arithmetic on the MMA issue path
+            // cost 3% at K = 1152 where no tile is narrow (profiles/r02_gemm_tuning.md)
             for (int t = pair; t < p.tiles; t += n_pairs) {
                 mbar_wait(&bars->tempty[acc], aph ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(acc * BN);
+                uint32_t idesc = idesc_full;
+                if constexpr (NARROW) {
+                    int tm, tn;
+                    tile_coords(t, p, tm, tn);
+                    if (tn == p.n_tiles - 1) idesc = idesc_last;
+                }
                 for (int kb = 0; kb < p.k_slabs; ++kb) {
                     mbar_wait(&bars->full[s], ph);
                     tc_fence_after();
@@ -251,11 +267,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint8_t* stage0 = smem + C::kEpi0 + g * kBufPerGroup * kStageBoxBytes;
         int acc = 0, box = 0;
         uint32_t aph = 0;
-        constexpr int kChunks = BN / 64;
         for (int t = pair; t < p.tiles; t += n_pairs) {
             int tm, tn;
             tile_coords(t, p, tm, tn);
             const int row0 = tm * 2 * kRowsCta + (int)rank * kRowsCta;
+            const int kChunks = ((NARROW && tn == p.n_tiles - 1) ? p.n_last : BN) / 64;
             mbar_wait(&bars->tfull[acc], aph);
             tc_fence_after();
 #pragma unroll 1
@@ -320,14 +336,21 @@ static bool map_2d(CUtensorMap* m, const void* base, int64_t inner, int64_t oute
 }
 
 static int g_sms = 0;
+// tuning knobs for A/B runs (scripts/bench_gemm.py): PAB_GEMM_GROUP = M tiles per raster
+// group
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+static int g_group = env_int("PAB_GEMM_GROUP", 8);
 
-template <int BN>
-static int launch(const void* A, int64_t lda, const void* B, int64_t ldb, void* Cp, int64_t ldc, int64_t M,
+template <int BN, bool NARROW>
+static int launch_t(const void* A, int64_t lda, const void* B, int64_t ldb, void* Cp, int64_t ldc, int64_t M,
                   int64_t N, int64_t K, int epilogue, cudaStream_t st) {
     using C = Cfg<BN>;
     static bool attr = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
+        if (cudaFuncSetAttribute(gemm_kernel<BN, NARROW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
             cudaSuccess)
             return launch_status("gemm smem attribute");
         attr = true;
@@ -338,10 +361,14 @@ static int launch(const void* A, int64_t lda, const void* B, int64_t ldb, void* 
         return PAB_ERR_CUDA;
     Params p;
     p.m_tiles = (int)((M + 2 * kRowsCta - 1) / (2 * kRowsCta));
-    p.n_tiles = (int)((N + BN - 1) / BN);  // a partial last N tile: B rows zero-filled, C columns clipped
+    p.n_tiles = (int)((N + BN - 1) / BN);
+    // last tile width rounded up to whole 64-column epilogue boxes (B rows past N zero-filled,
+    // C columns past N clipped by the tensor maps)
+    p.n_last = (int)(((N - (int64_t)(p.n_tiles - 1) * BN) + 63) / 64 * 64);
     p.k_slabs = (int)((K + kBK - 1) / kBK);
     p.tiles = p.m_tiles * p.n_tiles;
     p.epilogue = epilogue;
+    p.group = g_group;
     if (g_sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -349,8 +376,15 @@ static int launch(const void* A, int64_t lda, const void* B, int64_t ldb, void* 
     }
     int pairs = g_sms / 2;
     if (pairs > p.tiles) pairs = p.tiles;
-    gemm_kernel<BN><<<2 * pairs, kThreads, C::kSmem, st>>>(ma, mb, mc, p);
+    gemm_kernel<BN, NARROW><<<2 * pairs, kThreads, C::kSmem, st>>>(ma, mb, mc, p);
     return launch_status("gemm");
+}
+
+template <int BN>
+static int launch(const void* A, int64_t lda, const void* B, int64_t ldb, void* Cp, int64_t ldc, int64_t M,
+                  int64_t N, int64_t K, int epilogue, cudaStream_t st) {
+    return (N % BN) ? launch_t<BN, true>(A, lda, B, ldb, Cp, ldc, M, N, K, epilogue, st)
+                    : launch_t<BN, false>(A, lda, B, ldb, Cp, ldc, M, N, K, epilogue, st);
 }
 
 }  // namespace gemm
@@ -369,7 +403,11 @@ extern "C" int pab_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t 
         return PAB_ERR_UNSUPPORTED;
     if (M > 0x7fffffff || N > 0x7fffffff || K > 0x7fffffff) return PAB_ERR_UNSUPPORTED;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    if (N % 256 == 0 && N >= 4096) return launch<256>(A, lda, B, ldb, C, ldc, M, N, K, epilogue, st);
-    if (N % 192 == 0) return launch<192>(A, lda, B, ldb, C, ldc, M, N, K, epilogue, st);
-    return launch<128>(A, lda, B, ldb, C, ldc, M, N, K, epilogue, st);
+    // 256-wide tiles read the least shared memory per MMA (192: -6%, 128: -25% at N = 3456 / 4608,
+    // profiles/r02_gemm_tuning.md), with one narrower last tile for N % 256.  The static
+    // pair-strided order then leaves pairs unevenly loaded when the output has few tiles
+    // per row block (N = 1152: 4 x 256 + 128), so there uniform 192-wide tiles win.
+    if (N % 256 != 0 && N % 192 == 0 && N <= 1536)
+        return launch<192>(A, lda, B, ldb, C, ldc, M, N, K, epilogue, st);
+    return launch<256>(A, lda, B, ldb, C, ldc, M, N, K, epilogue, st);
 }
