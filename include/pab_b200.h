@@ -187,6 +187,20 @@ int pab_attention_select(const pab_attn_args* args);
 int pab_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                   int64_t M, int64_t N, int64_t K, int epilogue, void* stream);
 
+/*
+ * Output projection fused with the residual add of its site (the epilogue does the
+ * `x = x + o` of reference model.py:503 that the next site's prologue did before):
+ *   o[m, n] = bf16( sum_k A[m, k] * B[n, k] )          (as pab_gemm_bf16, epilogue 0)
+ *   x[perm(m), n] += o[m, n]                           (fp32, one rounding)
+ *   C[m, n] = o[m, n]   only if C != NULL (the site's output is cached for a later step)
+ * perm is the identity, or with tm_t, tm_s > 0 maps token-major GEMM rows (b, s, t) to
+ * frame-major residual rows (b, t, s) (the temporal site, S = tm_s, T = tm_t; M must be
+ * a multiple of tm_t * tm_s).  x: fp32, row stride ldx (elements, multiple of 4), N % 4 == 0.
+ */
+int pab_gemm_bf16_residual(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                           float* x, int64_t ldx, int64_t M, int64_t N, int64_t K,
+                           int64_t tm_t, int64_t tm_s, void* stream);
+
 /* Debug only: record a clock64 event timeline of CTA (0,0,0) of subsequent
  * tcgen05 attention launches into device_buffer (NULL disables). */
 int pab_attn_debug_trace(long long* device_buffer);

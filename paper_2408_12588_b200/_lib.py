@@ -71,6 +71,10 @@ SIGNATURES = {
     ),
     "pab_attention": (ctypes.c_int, [ctypes.POINTER(AttnArgs), ctypes.c_int, c_vp]),
     "pab_gemm_bf16": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, ctypes.c_int, c_vp]),
+    "pab_gemm_bf16_residual": (
+        ctypes.c_int,
+        [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp],
+    ),
     "pab_attention_select": (ctypes.c_int, [ctypes.POINTER(AttnArgs)]),
     "pab_attn_debug_trace": (ctypes.c_int, [c_vp]),
 }

@@ -69,6 +69,11 @@ struct Params {
     int n_last;    // width of the last N tile (a multiple of 64, <= BN): N = (n_tiles-1)*BN + n_last - pad
     int epilogue;
     int group;  // M tiles per raster group
+    // epilogue 2 (residual): x[perm(m), n] += bf16(acc); C written only if store_c
+    float* x;
+    int64_t ldx, M, N;
+    int64_t tm_t, tm_s;  // > 0: GEMM rows are token-major (b, s, t), x rows frame-major (b, t, s)
+    int store_c;
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -290,6 +295,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (p.epilogue == 1) {
 #pragma unroll
                     for (int i = 0; i < 64; ++i) v[i] = gelu_tanh(v[i]);
+                } else if (p.epilogue == 2) {
+                    // residual add of the site output into the fp32 stream (reference
+                    // model.py:503 x = x + o) -- the add the next site's prologue would do,
+                    // done here while the tensor cores work on the next tile
+#pragma unroll
+                    for (int i = 0; i < 64; ++i) v[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
+                    const int64_t grow = (int64_t)row0 + r;
+                    const int col0 = tn * BN + c * 64;
+                    if (grow < p.M && col0 < p.N) {
+                        int64_t xr = grow;
+                        if (p.tm_t > 0) {
+                            const int64_t per_b = p.tm_t * p.tm_s;
+                            const int64_t b = grow / per_b, rem = grow - b * per_b;
+                            const int64_t sidx = rem / p.tm_t, t = rem - sidx * p.tm_t;
+                            xr = (b * p.tm_t + t) * p.tm_s + sidx;
+                        }
+                        float4* xp = reinterpret_cast<float4*>(p.x + xr * p.ldx + col0);
+                        const int nv = min(64, (int)(p.N - col0)) >> 2;
+                        if (nv == 16) {
+                            float4 xv[16];
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) xv[j] = xp[j];
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                xv[j].x += v[4 * j]; xv[j].y += v[4 * j + 1];
+                                xv[j].z += v[4 * j + 2]; xv[j].w += v[4 * j + 3];
+                                xp[j] = xv[j];
+                            }
+                        } else {
+                            for (int j = 0; j < nv; ++j) {
+                                float4 xv = xp[j];
+                                xv.x += v[4 * j]; xv.y += v[4 * j + 1]; xv.z += v[4 * j + 2]; xv.w += v[4 * j + 3];
+                                xp[j] = xv;
+                            }
+                        }
+                    }
+                    if (!p.store_c) {
+                        if (++box == kBufPerGroup) box = 0;
+                        continue;
+                    }
                 }
                 uint8_t* sb = stage0 + box * kStageBoxBytes;
                 // the TMA store issued from this buffer kBufPerGroup boxes ago must have read it
@@ -344,9 +389,14 @@ static int env_int(const char* name, int dflt) {
 }
 static int g_group = env_int("PAB_GEMM_GROUP", 8);
 
+struct Resid {
+    float* x = nullptr;
+    int64_t ldx = 0, tm_t = 0, tm_s = 0;
+};
+
 template <int BN, bool NARROW>
 static int launch_t(const void* A, int64_t lda, const void* B, int64_t ldb, void* Cp, int64_t ldc, int64_t M,
-                  int64_t N, int64_t K, int epilogue, cudaStream_t st) {
+                    int64_t N, int64_t K, int epilogue, const Resid& rs, cudaStream_t st) {
     using C = Cfg<BN>;
     static bool attr = false;
     if (!attr) {
@@ -356,8 +406,11 @@ static int launch_t(const void* A, int64_t lda, const void* B, int64_t ldb, void
         attr = true;
     }
     CUtensorMap ma, mb, mc;
+    // epilogue 2 without an o output: the C map is never used (built over A)
+    const void* cbase = Cp ? Cp : A;
+    const int64_t cld = Cp ? ldc : lda;
     if (!map_2d(&ma, A, K, M, lda, kBK, kRowsCta) || !map_2d(&mb, B, K, N, ldb, kBK, BN / 2) ||
-        !map_2d(&mc, Cp, N, M, ldc, 64, kRowsCta))
+        !map_2d(&mc, cbase, Cp ? N : K, M, cld, 64, kRowsCta))
         return PAB_ERR_CUDA;
     Params p;
     p.m_tiles = (int)((M + 2 * kRowsCta - 1) / (2 * kRowsCta));
@@ -369,6 +422,13 @@ static int launch_t(const void* A, int64_t lda, const void* B, int64_t ldb, void
     p.tiles = p.m_tiles * p.n_tiles;
     p.epilogue = epilogue;
     p.group = g_group;
+    p.x = rs.x;
+    p.ldx = rs.ldx;
+    p.M = M;
+    p.N = N;
+    p.tm_t = rs.tm_t;
+    p.tm_s = rs.tm_s;
+    p.store_c = Cp != nullptr;
     if (g_sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -382,32 +442,63 @@ static int launch_t(const void* A, int64_t lda, const void* B, int64_t ldb, void
 
 template <int BN>
 static int launch(const void* A, int64_t lda, const void* B, int64_t ldb, void* Cp, int64_t ldc, int64_t M,
-                  int64_t N, int64_t K, int epilogue, cudaStream_t st) {
-    return (N % BN) ? launch_t<BN, true>(A, lda, B, ldb, Cp, ldc, M, N, K, epilogue, st)
-                    : launch_t<BN, false>(A, lda, B, ldb, Cp, ldc, M, N, K, epilogue, st);
+                  int64_t N, int64_t K, int epilogue, const Resid& rs, cudaStream_t st) {
+    return (N % BN) ? launch_t<BN, true>(A, lda, B, ldb, Cp, ldc, M, N, K, epilogue, rs, st)
+                    : launch_t<BN, false>(A, lda, B, ldb, Cp, ldc, M, N, K, epilogue, rs, st);
 }
 
-}  // namespace gemm
-}  // namespace pab
-
-extern "C" int pab_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
-                             int64_t M, int64_t N, int64_t K, int epilogue, void* stream) {
-    using namespace pab::gemm;
-    if (M < 0 || N <= 0 || K <= 0) return M == 0 ? PAB_OK : PAB_ERR_SHAPE;
-    if (M == 0) return PAB_OK;
-    if (!A || !B || !C) return PAB_ERR_INVALID;
-    if (epilogue != 0 && epilogue != 1) return PAB_ERR_INVALID;
-    if (lda < K || ldb < K || ldc < N) return PAB_ERR_SHAPE;
-    // TMA: 16-byte aligned bases and row strides (M, N and K tails are zero-filled / clipped)
-    if ((uintptr_t)A % 16 || (uintptr_t)B % 16 || (uintptr_t)C % 16 || lda % 8 || ldb % 8 || ldc % 8 || K % 8)
-        return PAB_ERR_UNSUPPORTED;
-    if (M > 0x7fffffff || N > 0x7fffffff || K > 0x7fffffff) return PAB_ERR_UNSUPPORTED;
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+static int dispatch(const void* A, int64_t lda, const void* B, int64_t ldb, void* Cp, int64_t ldc, int64_t M,
+                    int64_t N, int64_t K, int epilogue, const Resid& rs, cudaStream_t st) {
     // 256-wide tiles read the least shared memory per MMA (192: -6%, 128: -25% at N = 3456 / 4608,
     // profiles/r02_gemm_tuning.md), with one narrower last tile for N % 256.  The static
     // pair-strided order then leaves pairs unevenly loaded when the output has few tiles
     // per row block (N = 1152: 4 x 256 + 128), so there uniform 192-wide tiles win.
     if (N % 256 != 0 && N % 192 == 0 && N <= 1536)
-        return launch<192>(A, lda, B, ldb, C, ldc, M, N, K, epilogue, st);
-    return launch<256>(A, lda, B, ldb, C, ldc, M, N, K, epilogue, st);
+        return launch<192>(A, lda, B, ldb, Cp, ldc, M, N, K, epilogue, rs, st);
+    return launch<256>(A, lda, B, ldb, Cp, ldc, M, N, K, epilogue, rs, st);
+}
+
+}  // namespace gemm
+}  // namespace pab
+
+static int check_args(const void* A, int64_t lda, const void* B, int64_t ldb, const void* C, int64_t ldc,
+                      int64_t M, int64_t N, int64_t K) {
+    if (M < 0 || N <= 0 || K <= 0) return PAB_ERR_SHAPE;
+    if (!A || !B) return PAB_ERR_INVALID;
+    if (lda < K || ldb < K || (C && ldc < N)) return PAB_ERR_SHAPE;
+    // TMA: 16-byte aligned bases and row strides (M, N and K tails are zero-filled / clipped)
+    if ((uintptr_t)A % 16 || (uintptr_t)B % 16 || (uintptr_t)C % 16 || lda % 8 || ldb % 8 || (C && ldc % 8) ||
+        K % 8)
+        return PAB_ERR_UNSUPPORTED;
+    if (M > 0x7fffffff || N > 0x7fffffff || K > 0x7fffffff) return PAB_ERR_UNSUPPORTED;
+    return PAB_OK;
+}
+
+extern "C" int pab_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                             int64_t M, int64_t N, int64_t K, int epilogue, void* stream) {
+    using namespace pab::gemm;
+    if (M == 0) return PAB_OK;
+    if (!C) return PAB_ERR_INVALID;
+    const int st = check_args(A, lda, B, ldb, C, ldc, M, N, K);
+    if (st != PAB_OK) return st;
+    if (epilogue != 0 && epilogue != 1) return PAB_ERR_INVALID;
+    return dispatch(A, lda, B, ldb, C, ldc, M, N, K, epilogue, Resid{}, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int pab_gemm_bf16_residual(const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
+                                      int64_t ldc, float* x, int64_t ldx, int64_t M, int64_t N, int64_t K,
+                                      int64_t tm_t, int64_t tm_s, void* stream) {
+    using namespace pab::gemm;
+    if (M == 0) return PAB_OK;
+    const int st = check_args(A, lda, B, ldb, C, ldc, M, N, K);
+    if (st != PAB_OK) return st;
+    if (!x) return PAB_ERR_INVALID;
+    if (ldx < N || (uintptr_t)x % 16 || ldx % 4 || N % 4) return PAB_ERR_UNSUPPORTED;
+    if (tm_t < 0 || tm_s < 0 || (tm_t > 0) != (tm_s > 0) || (tm_t > 0 && M % (tm_t * tm_s))) return PAB_ERR_SHAPE;
+    Resid rs;
+    rs.x = x;
+    rs.ldx = ldx;
+    rs.tm_t = tm_t;
+    rs.tm_s = tm_s;
+    return dispatch(A, lda, B, ldb, C, ldc, M, N, K, 2, rs, reinterpret_cast<cudaStream_t>(stream));
 }

@@ -206,6 +206,33 @@ def gemm(a: torch.Tensor, w_t: torch.Tensor, out: torch.Tensor, epilogue: int = 
     return out
 
 
+def gemm_residual(a: torch.Tensor, w_t: torch.Tensor, x: torch.Tensor, out=None, token_major=None):
+    """x[perm(m)] += bf16(a @ w_t^T)[m] (fp32 residual stream, in place) and, when ``out`` is
+    given, out = bf16(a @ w_t^T) (the cached site output).  token_major = (T, S): the rows
+    of ``a`` are (b, s, t), the rows of ``x`` (b, t, s)."""
+    lib = _lib.load()
+    for t, name in ((a, "A"), (w_t, "B")):
+        _need(t, torch.bfloat16, name)
+        if t.dim() != 2 or t.stride(1) != 1:
+            raise ShapeError(f"gemm operand {name} must be 2-D with unit column stride")
+    _need(x, torch.float32, "residual")
+    M, K = a.shape
+    N = w_t.shape[0]
+    x2 = x.view(-1, x.shape[-1])
+    if w_t.shape[1] != K or x2.shape[1] != N or x2.shape[0] != M or x2.stride(1) != 1:
+        raise ShapeError(f"gemm_residual shapes {tuple(a.shape)} x {tuple(w_t.shape)}^T -> {tuple(x.shape)}")
+    if out is not None:
+        _need(out, torch.bfloat16, "C")
+        if out.shape != (M, N) or out.stride(1) != 1:
+            raise ShapeError("gemm_residual output must be (M, N) with unit column stride")
+    tm_t, tm_s = token_major if token_major is not None else (0, 0)
+    _lib.check(lib.pab_gemm_bf16_residual(a.data_ptr(), a.stride(0), w_t.data_ptr(), w_t.stride(0),
+                                          out.data_ptr() if out is not None else None,
+                                          out.stride(0) if out is not None else 0, x2.data_ptr(), x2.stride(0),
+                                          M, N, K, int(tm_t), int(tm_s), _stream()), "pab_gemm_bf16_residual")
+    return out
+
+
 def attn_args(q, k, v, o, qs, ks, vs, os_, n_a, n_b, n_q, n_k, heads, dh, scale=None) -> _lib.AttnArgs:
     """Build pab_attn_args; *s are (s_a, s_b, s_i) element strides of each operand."""
     for t, name in ((q, "q"), (k, "k"), (v, "v"), (o, "o")):

@@ -99,6 +99,7 @@ class StepContext:
         # the serial temporal site works token-major (rows (b, s, t)); its outputs carry a marker
         self.o_scratch_tm = torch.empty((rows, D), **bf)
         self.o_scratch_tm.pab_token_major = True
+        self._cross_slots = {}
         self.shape3 = (batch, self.T, self.S)
         self.launches = Launches()
         self.broadcast_object = "outputs"  # "scores": score broadcast (reference model.py:446-493)
@@ -121,9 +122,6 @@ class StepContext:
         null = [bool(np.all(ids_arr[b] < 0)) for b in range(batch)]
         n_null = sum(null)
         self.cross_live = batch - n_null if null[batch - n_null:] == [True] * n_null else batch
-        # scratch output of non-stored cross sites: only the live rows are ever written, so the
-        # null rows stay the zeros written here (no per-call memset)
-        self.o_scratch_cross = torch.zeros((self.rows, D), **bf) if self.cross_live < batch else None
         # per-run constants: text K/V of every cross site (step invariant)
         emb = embed_text(params, text_ids, batch).to(torch.bfloat16).reshape(batch * self.M, D)
         self.text_kv = []
@@ -137,6 +135,17 @@ class StepContext:
         self._build_attention_args()
         self._delta_in = None
         return self
+
+    def cross_slot(self, key):
+        """Per-(layer, block) cached-output slot of a cross site, zero-initialised once: its
+        null-text rows (exactly 0 in the reference) are never written, so they stay zero
+        across stores without a per-step memset.  A site's cache holds one entry, so the
+        slot can be overwritten in place whenever the site stores again."""
+        slot = self._cross_slots.get(key)
+        if slot is None:
+            slot = torch.zeros((self.rows, self.D), device=self.h.device, dtype=torch.bfloat16)
+            self._cross_slots[key] = slot
+        return slot
 
     def delta_in(self, r):
         """Copy of the residual at a Delta-DiT layer input (one reused fp32 buffer)."""
@@ -275,6 +284,29 @@ class _Step:
             self.trace.observe(TraceRecord(step=self.step, timestep=self.t, layer=li, kind=kind, block=block,
                                            decision=decision, source_step=source), o)
 
+    def wants_output(self) -> bool:
+        """A trace that digests / snapshots site outputs needs o even when it is not cached."""
+        return self.trace is not None and getattr(self.trace, "snapshot_mode", "none") in ("digest", "snapshot")
+
+    def out_gemm(self, a, w_t, store: bool, token_major: bool = False, rows=None, site=None):
+        """Output projection of a computed site fused with its residual add: the GEMM
+        epilogue does r += o (reference model.py:503) and writes o only when a later step
+        reuses it (or a trace digests it).  Called right after the site's prologue, so the
+        pending list is empty and r is the current stream."""
+        c = self.ctx
+        x = self.r.view(-1, c.D)
+        need = store or self.wants_output()
+        o = None
+        if need:
+            o = c.cross_slot(site) if site is not None and store else self.out_buffer(store, token_major)
+        tm = (c.T, c.S) if token_major else None
+        if rows is not None:
+            kernels.gemm_residual(a[:rows], w_t, x[:rows], None if o is None else o[:rows], token_major=tm)
+        else:
+            kernels.gemm_residual(a, w_t, x, o, token_major=tm)
+        self.added = True
+        return o
+
     def run_site(self, li, kind, block, compute, token_major=False, scores=None):
         """scores: (capture, replay) closures of an attention site in score-broadcast
         mode (reference model.py:469-499): a stored compute caches the bf16
@@ -284,13 +316,14 @@ class _Step:
         source = d.source(li, kind)
         site = (li, kind, block)
         c = self.ctx
+        self.added = False
         if source == self.step:
             store = d.should_store(li, kind)
             if scores is not None and store:
                 o, probs = scores[0](self.out_buffer(False, token_major))
                 self.cache.store(site, probs, self.step, "scores")
             else:
-                o = compute(self.out_buffer(store, token_major))
+                o = compute(store)
                 if store:
                     self.cache.store(site, o, self.step, "outputs")
             self.sink.site(kind, block)
@@ -307,7 +340,8 @@ class _Step:
                 o = entry.value
             c.launches.sites_reused += 1
             decision = "reuse"
-        self.pending.append(o)
+        if not self.added:
+            self.pending.append(o)
         self.record(li, kind, block, decision, source, o)
 
     # -- score broadcast (K10) ---------------------------------------------
@@ -400,49 +434,44 @@ class _Step:
     def attn_site(self, p, slot, temporal):
         c = self.ctx
 
-        def compute(o):
+        def compute(store):
             self.prologue(1, self.mods[self._li, slot], (p.ln_gamma, p.ln_beta), token_major=temporal)
             kernels.gemm(c.h, p.w_qkv_t, c.qkv)
             kernels.attention(c.args_temporal if temporal else c.args_spatial, c.attn_impl)
-            kernels.gemm(c.attn_out, p.wo_t, o)
             c.launches.attention_calls += 1
             c.launches.gemm_calls += 2
-            return o
+            return self.out_gemm(c.attn_out, p.wo_t, store, token_major=temporal)
 
         return compute
 
     def cross_site(self, p, blk):
         c = self.ctx
 
-        def compute(o):
+        def compute(store):
             self.prologue(2)
             rl = c.cross_live * c.T * c.S  # rows with non-null text (see StepContext.build)
-            zeroed = False
-            if o is c.o_scratch and c.o_scratch_cross is not None:
-                o, zeroed = c.o_scratch_cross, True  # null rows are permanently zero
-            if rl:
-                kernels.gemm(c.h[:rl], p.wq_t, c.qbuf[:rl])
-                kernels.attention(c.args_cross[self._li][blk], c.attn_impl)
-                kernels.gemm(c.attn_out[:rl], p.wo_t, o[:rl])
-                c.launches.attention_calls += 1
-                c.launches.gemm_calls += 2
-            if rl < c.rows and not zeroed:
-                o[rl:].zero_()  # null-text rows: the exact cross output (cached outputs only)
-            return o
+            if rl == 0:  # every row null: the output is exactly 0, nothing to add
+                self.added = True
+                return c.cross_slot((self._li, blk)) if (store or self.wants_output()) else None
+            kernels.gemm(c.h[:rl], p.wq_t, c.qbuf[:rl])
+            kernels.attention(c.args_cross[self._li][blk], c.attn_impl)
+            c.launches.attention_calls += 1
+            c.launches.gemm_calls += 2
+            # null-text rows of a cached output stay the zeros of its per-site slot
+            return self.out_gemm(c.attn_out, p.wo_t, store, rows=rl, site=(self._li, blk))
 
         return compute
 
     def mlp_site(self, p, slot):
         c = self.ctx
 
-        def compute(o):
+        def compute(store):
             self.prologue(1, self.mods[self._li, slot], (p.ln_gamma, p.ln_beta))
             # w1 GEMM with the tanh-GELU applied in its epilogue (no extra HBM pass over
-            # the 4D-wide hidden activation), then w2
+            # the 4D-wide hidden activation), then w2 with the residual add in its epilogue
             kernels.gemm(c.h, p.w1_t, c.hidden, kernels.EPI_GELU)
-            kernels.gemm(c.hidden, p.w2_t, o)
             c.launches.gemm_calls += 2
-            return o
+            return self.out_gemm(c.hidden, p.w2_t, store)
 
         return compute
 

@@ -57,3 +57,27 @@ def test_gemm_strided_operands():
     # A / C as column slices of wider rows (the fused [q|k|v] buffer, live-row views)
     _check(3000, 1152, 1152, lda=3456, ldc=3456)
     _check(777, 384, 1152, lda=1160, ldc=400)
+
+
+@pytest.mark.parametrize("M,N,K,store,tm", [(49920, 1152, 4608, False, None), (49920, 1152, 1152, True, None),
+                                            (4096, 1152, 1152, True, (16, 256)), (300, 144, 576, True, None),
+                                            (2048, 144, 144, False, (8, 128)), (24960, 1152, 1152, False, None)])
+def test_gemm_residual_epilogue(M, N, K, store, tm):
+    """x[perm(m)] += bf16(A B^T)[m] in the epilogue (the site output's residual add), with and
+    without the cached-output store, frame- and token-major rows."""
+    g = torch.Generator(device="cuda").manual_seed(1)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    w_t = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    x = torch.randn(M, N, device="cuda", generator=g)
+    x0 = x.clone()
+    out = torch.full((M, N), 5.0, device="cuda", dtype=torch.bfloat16) if store else None
+    kernels.gemm_residual(a, w_t, x, out, token_major=tm)
+    o = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    kernels.gemm(a, w_t, o)  # same tiles and accumulation order -> bitwise the same o
+    if store:
+        assert torch.equal(out, o)
+    o_rows = o.float()
+    if tm is not None:
+        T, S = tm
+        o_rows = o_rows.view(-1, S, T, N).permute(0, 2, 1, 3).reshape(M, N)
+    assert torch.equal(x, x0 + o_rows)
