@@ -43,12 +43,15 @@ constexpr int kProducerWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
 constexpr int kStageBoxBytes = kRowsCta * 128;  // 128 rows x 64 bf16 epilogue box
 static_assert(kEpiWarps == 4 || kEpiWarps == 8, "epilogue warps");
 
-template <int BN>
+constexpr int kXBoxBytes = kRowsCta * 128;   // 128 rows x 32 fp32 residual box
+template <int BN, bool RESID = false>
 struct Cfg {
     static constexpr int kABytes = kRowsCta * kBK * 2;          // 16 KB
     static constexpr int kBBytes = (BN / 2) * kBK * 2;          // BN/2 rows of B
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kEpiBytes = kEpiGroups * kBufPerGroup * kStageBoxBytes;
+    // RESID: per epilogue group, one 64-column fp32 residual chunk (two 32-column boxes)
+    static constexpr int kXBytes = RESID ? kEpiGroups * 2 * kXBoxBytes : 0;
+    static constexpr int kEpiBytes = kEpiGroups * kBufPerGroup * kStageBoxBytes + kXBytes;
     static constexpr int kStages = (232448 - kEpiBytes - 1280) / kStageBytes > 8
                                        ? 8 : (232448 - kEpiBytes - 1280) / kStageBytes;
     static constexpr int kRing = kStages * kStageBytes;
@@ -62,6 +65,7 @@ struct Cfg {
 
 struct Bars {
     uint64_t full[8], empty[8], tfull[2], tempty[2];
+    uint64_t xfull[2];  // RESID: residual chunk of epilogue group g landed
 };
 
 struct Params {
@@ -154,11 +158,12 @@ __device__ __forceinline__ void tile_coords(int t, const Params& p, int& m, int&
     n = r / gm;
 }
 
-template <int BN, bool NARROW>
+template <int BN, bool NARROW, bool RESID>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                const __grid_constant__ CUtensorMap map_c, const Params p) {
-    using C = Cfg<BN>;
+                const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_x,
+                const Params p) {
+    using C = Cfg<BN, RESID>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     Bars* bars = reinterpret_cast<Bars*>(smem + C::kBar0);
@@ -176,6 +181,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int a = 0; a < 2; ++a) {
             mbar_init(&bars->tfull[a], 1);
             mbar_init(&bars->tempty[a], 2 * kEpiWarps);  // both CTAs' epilogue warps
+            mbar_init(&bars->xfull[a], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -183,6 +189,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         prefetch_map(&map_a);
         prefetch_map(&map_b);
         prefetch_map(&map_c);
+        if (RESID) prefetch_map(&map_x);
     }
     if (warp == kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
@@ -272,11 +279,94 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint8_t* stage0 = smem + C::kEpi0 + g * kBufPerGroup * kStageBoxBytes;
         int acc = 0, box = 0;
         uint32_t aph = 0;
+        // ---- RESID: the residual add of the site output, x = x + o (reference model.py:503),
+        // done here instead of by the next site's prologue.  Each group streams its 64-column
+        // fp32 chunk of x through shared memory by TMA (two 32-column boxes, 128-byte swizzle):
+        // load (issued ahead: at tile start for the group's first chunk, right after the
+        // previous chunk's store otherwise), add the bf16-rounded o row by row (thread == row,
+        // like the accumulator), TMA-store back; o itself is stored only if p.store_c.
+        uint8_t* xbuf = smem + C::kEpi0 + kEpiGroups * kBufPerGroup * kStageBoxBytes + g * 2 * kXBoxBytes;
+        uint32_t xph = 0;
+        // x tensor-map coordinates of a 128-row block: frame-major (col, row); token-major
+        // (col, t = 0, s0, b) over the (D, T, S, B) view of the frame-major stream
+        auto x_coords = [&](int row0, int& c1, int& c2, int& c3) {
+            if (p.tm_t > 0) {
+                const int64_t per_b = p.tm_t * p.tm_s;
+                const int64_t b = row0 / per_b;
+                c1 = 0;
+                c2 = (int)((row0 - b * per_b) / p.tm_t);
+                c3 = (int)b;
+            } else {
+                c1 = row0; c2 = 0; c3 = 0;
+            }
+        };
+        auto x_load = [&](int col, int row0) {  // r == 0 only
+            bulk_wait_read<0>();  // the previous x / o stores of this group have read smem
+            int c1, c2, c3;
+            x_coords(row0, c1, c2, c3);
+            mbar_expect_tx(&bars->xfull[g], 2 * kXBoxBytes);
+            for (int h = 0; h < 2; ++h)
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(xbuf + h * kXBoxBytes)),
+                    "l"(reinterpret_cast<uint64_t>(&map_x)), "r"(smem_u32(&bars->xfull[g])), "r"(col + 32 * h),
+                    "r"(c1), "r"(c2), "r"(c3)
+                    : "memory");
+        };
+        auto resid_chunk = [&](float* v, int col, int row0, int next_col) {
+            // bf16 site output; the stream adds exactly the cached value
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
+            named_bar(1 + g, 128);  // r == 0 has waited for the previous stores (x_load)
+            if (p.store_c) {
+                const uint32_t rowaddr = smem_u32(stage0) + (uint32_t)r * 128;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    st_shared_v4(rowaddr + (uint32_t)(((j ^ (r & 7)) * 16)), pack_bf16(v[8 * j], v[8 * j + 1]),
+                                 pack_bf16(v[8 * j + 2], v[8 * j + 3]), pack_bf16(v[8 * j + 4], v[8 * j + 5]),
+                                 pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+            }
+            mbar_wait(&bars->xfull[g], xph);
+            xph ^= 1;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t rowaddr = smem_u32(xbuf + h * kXBoxBytes) + (uint32_t)r * 128;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t a = rowaddr + (uint32_t)(((j ^ (r & 7)) * 16));
+                    float4 xv;
+                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                 : "=f"(xv.x), "=f"(xv.y), "=f"(xv.z), "=f"(xv.w)
+                                 : "r"(a));
+                    const float* o = v + 32 * h + 4 * j;
+                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(xv.x + o[0]),
+                                 "f"(xv.y + o[1]), "f"(xv.z + o[2]), "f"(xv.w + o[3])
+                                 : "memory");
+                }
+            }
+            fence_async_smem();
+            named_bar(1 + g, 128);
+            if (r == 0) {
+                if (p.store_c) tma_store_2d(&map_c, stage0, col, row0);
+                int c1, c2, c3;
+                x_coords(row0, c1, c2, c3);
+                for (int h = 0; h < 2; ++h)
+                    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                                     reinterpret_cast<uint64_t>(&map_x)),
+                                 "r"(smem_u32(xbuf + h * kXBoxBytes)), "r"(col + 32 * h), "r"(c1), "r"(c2), "r"(c3)
+                                 : "memory");
+                bulk_commit();
+                if (next_col >= 0) x_load(next_col, row0);  // this group's next chunk of the tile
+            }
+        };
         for (int t = pair; t < p.tiles; t += n_pairs) {
             int tm, tn;
             tile_coords(t, p, tm, tn);
             const int row0 = tm * 2 * kRowsCta + (int)rank * kRowsCta;
             const int kChunks = ((NARROW && tn == p.n_tiles - 1) ? p.n_last : BN) / 64;
+            if constexpr (RESID) {
+                if (r == 0 && g < kChunks) x_load(tn * BN + g * 64, row0);  // before the accumulator is ready
+            }
             mbar_wait(&bars->tfull[acc], aph);
             tc_fence_after();
 #pragma unroll 1
@@ -295,46 +385,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (p.epilogue == 1) {
 #pragma unroll
                     for (int i = 0; i < 64; ++i) v[i] = gelu_tanh(v[i]);
-                } else if (p.epilogue == 2) {
-                    // residual add of the site output into the fp32 stream (reference
-                    // model.py:503 x = x + o) -- the add the next site's prologue would do,
-                    // done here while the tensor cores work on the next tile
-#pragma unroll
-                    for (int i = 0; i < 64; ++i) v[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
-                    const int64_t grow = (int64_t)row0 + r;
-                    const int col0 = tn * BN + c * 64;
-                    if (grow < p.M && col0 < p.N) {
-                        int64_t xr = grow;
-                        if (p.tm_t > 0) {
-                            const int64_t per_b = p.tm_t * p.tm_s;
-                            const int64_t b = grow / per_b, rem = grow - b * per_b;
-                            const int64_t sidx = rem / p.tm_t, t = rem - sidx * p.tm_t;
-                            xr = (b * p.tm_t + t) * p.tm_s + sidx;
-                        }
-                        float4* xp = reinterpret_cast<float4*>(p.x + xr * p.ldx + col0);
-                        const int nv = min(64, (int)(p.N - col0)) >> 2;
-                        if (nv == 16) {
-                            float4 xv[16];
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) xv[j] = xp[j];
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) {
-                                xv[j].x += v[4 * j]; xv[j].y += v[4 * j + 1];
-                                xv[j].z += v[4 * j + 2]; xv[j].w += v[4 * j + 3];
-                                xp[j] = xv[j];
-                            }
-                        } else {
-                            for (int j = 0; j < nv; ++j) {
-                                float4 xv = xp[j];
-                                xv.x += v[4 * j]; xv.y += v[4 * j + 1]; xv.z += v[4 * j + 2]; xv.w += v[4 * j + 3];
-                                xp[j] = xv;
-                            }
-                        }
-                    }
-                    if (!p.store_c) {
-                        if (++box == kBufPerGroup) box = 0;
-                        continue;
-                    }
+                }
+                if constexpr (RESID) {
+                    resid_chunk(v, tn * BN + c * 64, row0, c + kEpiGroups < kChunks ? tn * BN + (c + kEpiGroups) * 64 : -1);
+                    continue;
                 }
                 uint8_t* sb = stage0 + box * kStageBoxBytes;
                 // the TMA store issued from this buffer kBufPerGroup boxes ago must have read it
@@ -389,29 +443,55 @@ static int env_int(const char* name, int dflt) {
 }
 static int g_group = env_int("PAB_GEMM_GROUP", 8);
 
+static bool map_x4(CUtensorMap* m, float* x, int64_t N, int64_t M, int64_t ldx, int64_t tm_t, int64_t tm_s) {
+    auto encode = get_encode();
+    if (!encode) return false;
+    cuuint64_t dims[4], strides[3];
+    cuuint32_t box[4];
+    const cuuint64_t row = (cuuint64_t)ldx * 4;
+    if (tm_t > 0) {  // (D, T, S, B) view of the frame-major stream, box = 32 cols x T x 128/T tokens
+        dims[0] = N; dims[1] = tm_t; dims[2] = tm_s; dims[3] = M / (tm_t * tm_s);
+        strides[0] = row * tm_s; strides[1] = row; strides[2] = row * tm_t * tm_s;
+        box[0] = 32; box[1] = (cuuint32_t)tm_t; box[2] = (cuuint32_t)(kRowsCta / tm_t); box[3] = 1;
+    } else {
+        dims[0] = N; dims[1] = M; dims[2] = 1; dims[3] = 1;
+        strides[0] = row; strides[1] = row * M; strides[2] = row * M;
+        box[0] = 32; box[1] = kRowsCta; box[2] = 1; box[3] = 1;
+    }
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, x, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 struct Resid {
     float* x = nullptr;
     int64_t ldx = 0, tm_t = 0, tm_s = 0;
 };
 
-template <int BN, bool NARROW>
+template <int BN, bool NARROW, bool RESID>
 static int launch_t(const void* A, int64_t lda, const void* B, int64_t ldb, void* Cp, int64_t ldc, int64_t M,
                     int64_t N, int64_t K, int epilogue, const Resid& rs, cudaStream_t st) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, RESID>;
     static bool attr = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(gemm_kernel<BN, NARROW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
-            cudaSuccess)
+        if (cudaFuncSetAttribute(gemm_kernel<BN, NARROW, RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::kSmem) != cudaSuccess)
             return launch_status("gemm smem attribute");
         attr = true;
     }
-    CUtensorMap ma, mb, mc;
-    // epilogue 2 without an o output: the C map is never used (built over A)
+    CUtensorMap ma, mb, mc, mx;
+    // residual epilogue without an o output: the C map is never used (built over A)
     const void* cbase = Cp ? Cp : A;
     const int64_t cld = Cp ? ldc : lda;
     if (!map_2d(&ma, A, K, M, lda, kBK, kRowsCta) || !map_2d(&mb, B, K, N, ldb, kBK, BN / 2) ||
         !map_2d(&mc, cbase, Cp ? N : K, M, cld, 64, kRowsCta))
         return PAB_ERR_CUDA;
+    if (RESID) {
+        if (!map_x4(&mx, rs.x, N, M, rs.ldx, rs.tm_t, rs.tm_s)) return PAB_ERR_CUDA;
+    } else {
+        mx = ma;  // unused
+    }
     Params p;
     p.m_tiles = (int)((M + 2 * kRowsCta - 1) / (2 * kRowsCta));
     p.n_tiles = (int)((N + BN - 1) / BN);
@@ -436,17 +516,18 @@ static int launch_t(const void* A, int64_t lda, const void* B, int64_t ldb, void
     }
     int pairs = g_sms / 2;
     if (pairs > p.tiles) pairs = p.tiles;
-    gemm_kernel<BN, NARROW><<<2 * pairs, kThreads, C::kSmem, st>>>(ma, mb, mc, p);
+    gemm_kernel<BN, NARROW, RESID><<<2 * pairs, kThreads, C::kSmem, st>>>(ma, mb, mc, mx, p);
     return launch_status("gemm");
 }
 
-template <int BN>
+template <int BN, bool RESID>
 static int launch(const void* A, int64_t lda, const void* B, int64_t ldb, void* Cp, int64_t ldc, int64_t M,
                   int64_t N, int64_t K, int epilogue, const Resid& rs, cudaStream_t st) {
-    return (N % BN) ? launch_t<BN, true>(A, lda, B, ldb, Cp, ldc, M, N, K, epilogue, rs, st)
-                    : launch_t<BN, false>(A, lda, B, ldb, Cp, ldc, M, N, K, epilogue, rs, st);
+    return (N % BN) ? launch_t<BN, true, RESID>(A, lda, B, ldb, Cp, ldc, M, N, K, epilogue, rs, st)
+                    : launch_t<BN, false, RESID>(A, lda, B, ldb, Cp, ldc, M, N, K, epilogue, rs, st);
 }
 
+template <bool RESID>
 static int dispatch(const void* A, int64_t lda, const void* B, int64_t ldb, void* Cp, int64_t ldc, int64_t M,
                     int64_t N, int64_t K, int epilogue, const Resid& rs, cudaStream_t st) {
     // 256-wide tiles read the least shared memory per MMA (192: -6%, 128: -25% at N = 3456 / 4608,
@@ -454,8 +535,8 @@ static int dispatch(const void* A, int64_t lda, const void* B, int64_t ldb, void
     // pair-strided order then leaves pairs unevenly loaded when the output has few tiles
     // per row block (N = 1152: 4 x 256 + 128), so there uniform 192-wide tiles win.
     if (N % 256 != 0 && N % 192 == 0 && N <= 1536)
-        return launch<192>(A, lda, B, ldb, Cp, ldc, M, N, K, epilogue, rs, st);
-    return launch<256>(A, lda, B, ldb, Cp, ldc, M, N, K, epilogue, rs, st);
+        return launch<192, RESID>(A, lda, B, ldb, Cp, ldc, M, N, K, epilogue, rs, st);
+    return launch<256, RESID>(A, lda, B, ldb, Cp, ldc, M, N, K, epilogue, rs, st);
 }
 
 }  // namespace gemm
@@ -482,7 +563,7 @@ extern "C" int pab_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t 
     const int st = check_args(A, lda, B, ldb, C, ldc, M, N, K);
     if (st != PAB_OK) return st;
     if (epilogue != 0 && epilogue != 1) return PAB_ERR_INVALID;
-    return dispatch(A, lda, B, ldb, C, ldc, M, N, K, epilogue, Resid{}, reinterpret_cast<cudaStream_t>(stream));
+    return dispatch<false>(A, lda, B, ldb, C, ldc, M, N, K, epilogue, Resid{}, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int pab_gemm_bf16_residual(const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
@@ -495,10 +576,12 @@ extern "C" int pab_gemm_bf16_residual(const void* A, int64_t lda, const void* B,
     if (!x) return PAB_ERR_INVALID;
     if (ldx < N || (uintptr_t)x % 16 || ldx % 4 || N % 4) return PAB_ERR_UNSUPPORTED;
     if (tm_t < 0 || tm_s < 0 || (tm_t > 0) != (tm_s > 0) || (tm_t > 0 && M % (tm_t * tm_s))) return PAB_ERR_SHAPE;
+    // token-major rows: every 128-row block must be whole tokens of one batch entry
+    if (tm_t > 0 && (128 % tm_t || (tm_t * tm_s) % 128)) return PAB_ERR_UNSUPPORTED;
     Resid rs;
     rs.x = x;
     rs.ldx = ldx;
     rs.tm_t = tm_t;
     rs.tm_s = tm_s;
-    return dispatch(A, lda, B, ldb, C, ldc, M, N, K, 2, rs, reinterpret_cast<cudaStream_t>(stream));
+    return dispatch<true>(A, lda, B, ldb, C, ldc, M, N, K, 2, rs, reinterpret_cast<cudaStream_t>(stream));
 }

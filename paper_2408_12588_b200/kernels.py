@@ -206,6 +206,12 @@ def gemm(a: torch.Tensor, w_t: torch.Tensor, out: torch.Tensor, epilogue: int = 
     return out
 
 
+def residual_token_major_ok(T: int, S: int) -> bool:
+    """gemm_residual's token-major row map needs every 128-row block to be whole tokens
+    of one batch entry: T | 128 and 128 | T*S (C3: T = 16, S = 1560)."""
+    return 128 % T == 0 and (T * S) % 128 == 0
+
+
 def gemm_residual(a: torch.Tensor, w_t: torch.Tensor, x: torch.Tensor, out=None, token_major=None):
     """x[perm(m)] += bf16(a @ w_t^T)[m] (fp32 residual stream, in place) and, when ``out`` is
     given, out = bf16(a @ w_t^T) (the cached site output).  token_major = (T, S): the rows

@@ -289,11 +289,20 @@ class _Step:
         return self.trace is not None and getattr(self.trace, "snapshot_mode", "none") in ("digest", "snapshot")
 
     def out_gemm(self, a, w_t, store: bool, token_major: bool = False, rows=None, site=None):
-        """Output projection of a computed site fused with its residual add: the GEMM
-        epilogue does r += o (reference model.py:503) and writes o only when a later step
-        reuses it (or a trace digests it).  Called right after the site's prologue, so the
-        pending list is empty and r is the current stream."""
+        """Output projection of a computed attention site fused with its residual add: the
+        GEMM epilogue does r += o (reference model.py:503) and writes o only when a later
+        step reuses it (or a trace digests it).  Called right after the site's prologue, so
+        the pending list is empty and r is the current stream.  (C3: the next prologue then
+        moves 6E instead of 12E bytes; measured 3.5% per video.  The MLP's w2 GEMM keeps the
+        plain epilogue: at K = 4D the residual variant's shallower smem ring cost more than
+        the prologue saved, profiles/r02_gemm_tuning.md.)"""
         c = self.ctx
+        if token_major and not kernels.residual_token_major_ok(c.T, c.S):
+            # no whole-token 128-row blocks: plain GEMM, the next prologue adds o (token-major
+            # pending term) as before
+            o = self.out_buffer(store, token_major)
+            kernels.gemm(a, w_t, o)
+            return o
         x = self.r.view(-1, c.D)
         need = store or self.wants_output()
         o = None
@@ -468,10 +477,12 @@ class _Step:
         def compute(store):
             self.prologue(1, self.mods[self._li, slot], (p.ln_gamma, p.ln_beta))
             # w1 GEMM with the tanh-GELU applied in its epilogue (no extra HBM pass over
-            # the 4D-wide hidden activation), then w2 with the residual add in its epilogue
+            # the 4D-wide hidden activation), then w2; the next prologue adds o
             kernels.gemm(c.h, p.w1_t, c.hidden, kernels.EPI_GELU)
+            o = self.out_buffer(store)
+            kernels.gemm(c.hidden, p.w2_t, o)
             c.launches.gemm_calls += 2
-            return self.out_gemm(c.hidden, p.w2_t, store)
+            return o
 
         return compute
 

@@ -36,6 +36,7 @@ o3 = torch.empty(rows, 3 * D, **bf)
 o1 = torch.empty(rows, D, **bf)
 o4 = torch.empty(rows, R, **bf)
 tq, to, t1, t2 = (w.t().contiguous() for w in (wqkv, wo, w1, w2))
+xres = torch.zeros(rows, D, device="cuda")
 res = {}
 for name, fn, fl in [
     ("qkv_cublas", lambda: torch.mm(h, wqkv, out=o3), 2 * rows * D * 3 * D),
@@ -46,6 +47,10 @@ for name, fn, fl in [
     ("w1_gelu_ours", lambda: kernels.gemm(h, t1, o4, kernels.EPI_GELU), 2 * rows * D * R),
     ("w2_cublas", lambda: torch.mm(hid, w2, out=o1), 2 * rows * R * D),
     ("w2_ours", lambda: kernels.gemm(hid, t2, o1), 2 * rows * R * D),
+    ("o_resid_ours", lambda: kernels.gemm_residual(h, to, xres), 2 * rows * D * D),
+    ("o_resid_store_ours", lambda: kernels.gemm_residual(h, to, xres, o1), 2 * rows * D * D),
+    ("o_resid_tm_ours", lambda: kernels.gemm_residual(h, to, xres, None, token_major=(16, 1560)), 2 * rows * D * D),
+    ("w2_resid_ours", lambda: kernels.gemm_residual(hid, t2, xres), 2 * rows * R * D),
 ]:
     s = t(fn)
     res[name] = {"ms": round(s * 1e3, 4), "tflops": round(fl / s / 1e12, 1)}
