@@ -368,6 +368,9 @@ def main():
         return a.elapsed_time(b) / reps / 1000.0
 
     B, T, S, D, M = ctx.B, ctx.T, ctx.S, ctx.D, ctx.M
+    comp = table.compute_mask()  # (steps, layers, kind) spatial, temporal, cross, mlp
+    site_counts = (int(comp[:, :, 0].sum()), int(comp[:, :, 1].sum()),
+                   int(comp[:, :, 2].sum()) * (2 if cfg.cross_in_temporal else 1), int(comp[:, :, 3].sum()) * 2)
     flop_sp = 4.0 * B * T * S * S * D
     flop_tm = 4.0 * B * S * T * T * D
     Bc = getattr(ctx, "cross_live", B)  # cross sites skip null-text (unconditional CFG) rows: exactly 0
@@ -383,8 +386,41 @@ def main():
         t_tm = time_launch(lambda: kernels.attention(ctx.args_temporal))
         t_cr = time_launch(lambda: kernels.attention(ctx.args_cross[0][0]))
         t_mn = time_launch(lambda: kernels.residual_modnorm(xbuf, xbuf, pend, h_out=ctx.h, mod=mod, mode=1))
+        # projection GEMMs (csrc/gemm.cu) on the engine's workspaces with layer-0 weights
+        lp = params.layers[0]
+        rl = Bc * T * S
+        g_ms = {
+            "qkv": time_launch(lambda: kernels.gemm(ctx.h, lp.spatial.w_qkv_t, ctx.qkv)),
+            "o_resid": time_launch(lambda: kernels.gemm_residual(ctx.attn_out, lp.spatial.wo_t, xbuf)),
+            "cross_q": time_launch(lambda: kernels.gemm(ctx.h[:rl], lp.cross_spatial.wq_t, ctx.qbuf[:rl])),
+            "cross_o_resid": time_launch(lambda: kernels.gemm_residual(ctx.attn_out[:rl], lp.cross_spatial.wo_t,
+                                                                       xbuf[:rl])),
+            "w1_gelu": time_launch(lambda: kernels.gemm(ctx.h, lp.mlp_spatial.w1_t, ctx.hidden, kernels.EPI_GELU)),
+            "w2": time_launch(lambda: kernels.gemm(ctx.hidden, lp.mlp_spatial.w2_t, ctx.attn_out)),
+        }
         del xbuf, pend
+        R = cfg.mlp_hidden
+        g_flops = {"qkv": 2.0 * rows * D * 3 * D, "o_resid": 2.0 * rows * D * D, "cross_q": 2.0 * rl * D * D,
+                   "cross_o_resid": 2.0 * rl * D * D, "w1_gelu": 2.0 * rows * D * R, "w2": 2.0 * rows * R * D}
+        # launches per video: spatial + temporal computes run qkv + o; cross computes q + o; mlp w1 + w2
+        n_sp, n_tm, n_cr, n_ml = site_counts
+        g_count = {"qkv": n_sp + n_tm, "o_resid": n_sp + n_tm, "cross_q": n_cr, "cross_o_resid": n_cr,
+                   "w1_gelu": n_ml, "w2": n_ml}
+        gemm = {k: {"ms": g_ms[k] * 1e3, "tflops": g_flops[k] / g_ms[k] / 1e12,
+                    "frac_bf16_peak": g_flops[k] / g_ms[k] / 1e12 / peak_tf, "launches_per_video": g_count[k]}
+                for k in g_ms}
+        g_time = sum(g_ms[k] * g_count[k] for k in g_ms)
+        g_fl = sum(g_flops[k] * g_count[k] for k in g_ms)
+        gemm["all_projections"] = {"tflops": g_fl / g_time / 1e12, "frac_bf16_peak": g_fl / g_time / 1e12 / peak_tf,
+                                   "s_per_video": g_time, "note": "time-weighted over the video's launches"}
+        a_time = n_sp * t_sp + n_tm * t_tm + n_cr * t_cr
+        a_fl = n_sp * flop_sp + n_tm * flop_tm + n_cr * flop_cr
+        attn_agg = {"tflops": a_fl / a_time / 1e12, "frac_bf16_peak": a_fl / a_time / 1e12 / peak_tf,
+                    "s_per_video": a_time, "note": "spatial + temporal + cross attention launches of one video, "
+                    "algorithmic flops (cross: live CFG rows) / their measured time"}
         return t_sp, {
+            "gemm": gemm,
+            "attention_aggregate": attn_agg,
             "spatial_attn": {"ms": t_sp * 1e3, "tflops": flop_sp / t_sp / 1e12,
                              "frac_bf16_peak": flop_sp / t_sp / 1e12 / peak_tf},
             "temporal_attn": {"ms": t_tm * 1e3, "gbs": 8.0 * B * T * S * D / t_tm / 1e9,
@@ -465,21 +501,25 @@ def main():
         del den_none
 
     t_sp_step, kern_step = kernel_times(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
-    achieved = flop_sp / t_sp / 1e12
+    # roofline of the dominant kernel: the projection GEMM (gemm_kernel, ~60% of the video);
+    # the MLP w2 launch is its largest single share (rows x 4D x D, 530 GFLOP at C3)
+    w2 = kern["gemm"]["w2"]
+    achieved = w2["tflops"]
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01_attn_fa_ncu_full.json")
+    prof = os.path.join(ROOT, "profiles", "r02_gemm_w2_ncu.json")
     if os.path.exists(prof) and args.config == "C3":
-        caps = json.load(open(prof))
-        # ncu raw page reports dram__bytes_{read,write}.sum in Mbyte; per launch
-        traffic = statistics.mean(c["dram__bytes_read.sum"] + c["dram__bytes_write.sum"] for c in caps
-                                  if c.get("site", "spatial") == "spatial") * 1e6
+        cap = json.load(open(prof))
+        traffic = cap["dram_bytes_per_launch"]
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
-                "traffic_note": "DRAM bytes per launch from profiles/r01_attn_fa_ncu_full.json (ncu --set full); "
-                                "algorithmic bytes 8*E = 460 MB (Q,K,V read + O write, bf16)",
-                "kernel": "attn_fa_kernel (spatial)",
+                "traffic_note": "DRAM bytes per launch from profiles/r02_gemm_w2_ncu.json (ncu --set full); "
+                                "algorithmic bytes: A 460 MB + W 10.6 MB read, C 115 MB written",
+                "kernel": "gemm_kernel (MLP w2 projection, tcgen05 2-CTA)",
                 "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
-                "algorithmic_flops_per_launch": flop_sp}
+                "algorithmic_flops_per_launch": 2.0 * ctx.rows * cfg.mlp_hidden * D,
+                "all_projection_gemms_frac": kern["gemm"]["all_projections"]["frac_bf16_peak"],
+                "attention_aggregate_frac": kern["attention_aggregate"]["frac_bf16_peak"],
+                "spatial_attention_frac": kern["spatial_attn"]["frac_bf16_peak"]}
     flops_pab, _ = video_flops(cfg, table, c["batch"])
 
     if rank == 0:

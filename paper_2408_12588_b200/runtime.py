@@ -70,7 +70,8 @@ class Launches:
     log: list = field(default_factory=list)  # (step, layer, kind, block, decision, source)
 
     def own_kernels(self) -> int:
-        return self.attention_calls + self.prologue_calls + self.other_calls
+        # every launch is the library's own kernel: attention, prologue/epilogue, GEMM, DDIM
+        return self.attention_calls + self.prologue_calls + self.gemm_calls + self.other_calls
 
 
 class StepContext:
