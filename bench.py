@@ -501,25 +501,30 @@ def main():
         del den_none
 
     t_sp_step, kern_step = kernel_times(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
-    # roofline of the dominant kernel: the projection GEMM (gemm_kernel, ~60% of the video);
-    # the MLP w2 launch is its largest single share (rows x 4D x D, 530 GFLOP at C3)
-    w2 = kern["gemm"]["w2"]
+    # roofline of the dominant kernel: the projection GEMM (gemm_kernel, ~65% of the video);
+    # the MLP w2 launch is its largest single share (rows x 4D x D, 530 GFLOP at C3).  Timed
+    # back to back right after the timed videos (power-capped clocks, as inside a video) and
+    # set against the SUSTAINED bf16 peak; the burst timings (after a cool-down, short bursts
+    # at up to 1965 MHz) are in "kernels" and can exceed the burst cuBLAS reference
+    w2 = kern_step["gemm"]["w2"]
     achieved = w2["tflops"]
+    peak_rf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     traffic = None
     prof = os.path.join(ROOT, "profiles", "r02_gemm_w2_ncu.json")
     if os.path.exists(prof) and args.config == "C3":
         cap = json.load(open(prof))
         traffic = cap["dram_bytes_per_launch"]
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_rf, "unit": "TFLOP/s",
+                "frac": achieved / peak_rf, "traffic": traffic,
                 "traffic_note": "DRAM bytes per launch from profiles/r02_gemm_w2_ncu.json (ncu --set full); "
                                 "algorithmic bytes: A 460 MB + W 10.6 MB read, C 115 MB written",
                 "kernel": "gemm_kernel (MLP w2 projection, tcgen05 2-CTA)",
-                "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
+                "peak_source": f"{peak_src} bf16 sustained (MEASURED_PEAKS.json)",
                 "algorithmic_flops_per_launch": 2.0 * ctx.rows * cfg.mlp_hidden * D,
-                "all_projection_gemms_frac": kern["gemm"]["all_projections"]["frac_bf16_peak"],
-                "attention_aggregate_frac": kern["attention_aggregate"]["frac_bf16_peak"],
-                "spatial_attention_frac": kern["spatial_attn"]["frac_bf16_peak"]}
+                "all_projection_gemms_frac": kern_step["gemm"]["all_projections"]["frac_bf16_peak"],
+                "attention_aggregate_frac": kern_step["attention_aggregate"]["frac_bf16_peak"],
+                "spatial_attention_frac": kern_step["spatial_attn"]["frac_bf16_peak"],
+                "spatial_attention_frac_burst": kern["spatial_attn"]["frac_bf16_peak"]}
     flops_pab, _ = video_flops(cfg, table, c["batch"])
 
     if rank == 0:
