@@ -340,7 +340,10 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    use_graph = world == 1 and not args.no_graph
+    # one CUDA graph per video; under torchrun with NCCL the all-to-alls are captured too
+    # (a gloo group -- several ranks sharing one GPU in tests -- cannot be captured)
+    backend = os.environ.get("PAB_DIST_BACKEND", "nccl")
+    use_graph = not args.no_graph and (world == 1 or backend == "nccl")
 
     def denoise(d, zz):
         return d.run_graph(zz) if use_graph else d.run(zz)
@@ -434,8 +437,13 @@ def main():
         }
 
     one_video()
+    graph_note = None
     if use_graph:
-        den.capture_graph()  # the whole 30-step loop as one CUDA graph (static decision table)
+        try:
+            den.capture_graph()  # the whole 30-step loop as one CUDA graph (static decision table)
+        except Exception as e:  # keep the bench line: report eager launching and why
+            use_graph, graph_note = False, f"graph capture failed, eager: {e!r}"[:200]
+            torch.cuda.synchronize()
     barrier()
     time.sleep(3.0)  # let the board's power average settle (sw_power_cap window) -> burst clocks
     t_sp, kern = kernel_times(peaks["bf16_tflops"])
@@ -474,6 +482,32 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     io_bytes = x_dev.numel() * x_dev.element_size()  # this rank's share of the latent, each way
+
+    # all-to-all traffic of one video: calls and bytes from the run's
+    # ledger, the per-call time from the same exchange timed alone (CUDA events, max over ranks)
+    a2a = None
+    if world > 1 and getattr(den, "hook", None) is not None:
+        hook = den.hook
+        calls = den.ledger.event_count() // (2 if split else 1)
+        send_b = hook.h_send.numel() * hook.h_send.element_size()
+        from paper_2408_12588_b200.parallel import exchange_frames_to_tokens
+
+        exchange_frames_to_tokens(hook.h_send, hook.h_tok, hook.group)
+        barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(20):
+            exchange_frames_to_tokens(hook.h_send, hook.h_tok, hook.group)
+        a1.record(stream)
+        barrier()
+        a_ms = a0.elapsed_time(a1) / 20
+        t = torch.tensor([a_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        a_ms = float(t.item())
+        a2a = {"calls_per_video": calls, "bytes_per_call_per_rank": send_b,
+               "wire_bytes_per_call_per_rank": hook.wire, "ms_per_call": a_ms,
+               "est_ms_per_video": a_ms * calls, "skipped_on_temporal_broadcast_steps": True,
+               "ledger_elements_per_video": den.ledger.total_elements()}
 
     # no-PAB reference point (same engine, every site computed)
     none_ms = None
@@ -540,7 +574,8 @@ def main():
                        "parallelism": (f"cfg2x_broadcast_sp{world // 2}" if split else
                                        f"broadcast_sp{world}" if world > 1 else "single"),
                        "l2": "inputs larger than L2 (fp32 latent 230 MB > 126 MB L2)",
-                       "launch": "one CUDA graph per video (static decision table)" if use_graph else "eager",
+                       "launch": ("one CUDA graph per video (static decision table)" if use_graph
+                                  else graph_note or "eager"),
                        "none_s_per_video": None if none_ms is None else none_ms / 1000.0,
                        "pab_speedup_vs_none": None if none_ms is None else none_ms / ms,
                        "video_tflop_pab": flops_pab / 1e12, "achieved_tflops_video": flops_pab / (ms / 1e3) / 1e12,
@@ -549,6 +584,7 @@ def main():
             "e2e": {"value": e2e_ms / 1000.0, "unit": "s/video", "h2d_bytes_per_step": io_bytes,
                     "d2h_bytes_per_step": io_bytes},
             "gpu_launches": launches,
+            "alltoall": a2a,
             "roofline": roofline,
             "kernels": kern,
             "kernels_in_step": dict(kern_step, note="same launches after the timed videos (power-capped "

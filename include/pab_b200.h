@@ -89,6 +89,28 @@ int pab_residual_modnorm_tm(const float* x_in, float* x_out,
                             int D, float eps, int mode, int h_token_major, void* stream);
 
 /*
+ * General form of the three prologues above (they are special cases of it): every
+ * pending term and the h output carry a row layout over the (n_b, n_t, n_s) block of
+ * the residual stream:
+ *   PAB_LAYOUT_FRAME  rows (b, t, s)                          the stream's own order
+ *   PAB_LAYOUT_TOKEN  rows (b, s, t)                          the temporal site's order
+ *   PAB_LAYOUT_A2A    rows (s / (n_s/n_w), t, b, s % (n_s/n_w)) a frame shard in the
+ *                     sequence-parallel all-to-all order (n_s % n_w == 0)
+ * so the temporal site's received output is added by the next prologue straight from
+ * the all-to-all receive buffer (no unpack pass; reference parallel.reshard,
+ * pkg/src/pab_engine/parallel.py:140-180, 335-340).  term_layout may be NULL (all FRAME).
+ */
+#define PAB_LAYOUT_FRAME 0
+#define PAB_LAYOUT_TOKEN 1
+#define PAB_LAYOUT_A2A 2
+int pab_residual_modnorm_ex(const float* x_in, float* x_out,
+                            const void* const* pending, const int* term_layout, int n_pending,
+                            const float* gamma, const float* beta,
+                            const float* mod, void* h_out,
+                            int64_t n_b, int64_t n_t, int64_t n_s, int64_t n_w,
+                            int D, float eps, int mode, int h_layout, void* stream);
+
+/*
  * Fused end-of-step residual drain + classifier-free guidance + DDIM (K8).
  * Replaces: the eps combine and ddim_update of diffusion.sample
  * (pkg/src/pab_engine/diffusion.py:183-189, 100-103).

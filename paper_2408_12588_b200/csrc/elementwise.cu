@@ -347,10 +347,13 @@ __global__ void fill_uniform_kernel(void* dst, int dtype, int64_t rows, int64_t 
 
 using namespace pab;
 
-// token-major source layout of the pending terms (bit i: term i stored (b, s, t))
+// source layouts of the pending terms: bit i of `mask` -> term i token-major (b, s, t),
+// bit i of `a2a` -> term i in all-to-all order over n_w ranks
 struct TmState {
     uint32_t mask;
     int64_t t, s;
+    uint32_t a2a = 0;
+    int64_t n_b = 1, n_w = 1;
 };
 static int residual_modnorm_impl(const float* x_in, float* x_out, const void* const* pending,
                                  int n_pending, const float* gamma, const float* beta,
@@ -388,6 +391,31 @@ extern "C" int pab_residual_modnorm_tm(const float* x_in, float* x_out, const vo
                                  RowPerm{n_b, n_t, n_s, h_token_major ? -1 : 0}, tm, stream);
 }
 
+extern "C" int pab_residual_modnorm_ex(const float* x_in, float* x_out, const void* const* pending,
+                                       const int* term_layout, int n_pending, const float* gamma,
+                                       const float* beta, const float* mod, void* h_out, int64_t n_b,
+                                       int64_t n_t, int64_t n_s, int64_t n_w, int D, float eps, int mode,
+                                       int h_layout, void* stream) {
+    if (n_b < 1 || n_t < 1 || n_s < 1 || n_w < 1) return PAB_ERR_SHAPE;
+    if (n_pending < 0 || n_pending > PAB_MAX_PENDING) return PAB_ERR_SHAPE;
+    TmState tm{0u, n_t, n_s};
+    tm.n_b = n_b;
+    tm.n_w = n_w;
+    bool a2a = h_layout == PAB_LAYOUT_A2A;
+    for (int i = 0; i < n_pending; ++i) {
+        const int l = term_layout ? term_layout[i] : PAB_LAYOUT_FRAME;
+        if (l == PAB_LAYOUT_TOKEN) tm.mask |= 1u << i;
+        else if (l == PAB_LAYOUT_A2A) { tm.a2a |= 1u << i; a2a = true; }
+        else if (l != PAB_LAYOUT_FRAME) return PAB_ERR_INVALID;
+    }
+    if (a2a && n_s % n_w != 0) return PAB_ERR_SHAPE;
+    if (h_layout < PAB_LAYOUT_FRAME || h_layout > PAB_LAYOUT_A2A) return PAB_ERR_INVALID;
+    if (h_layout == PAB_LAYOUT_A2A && mode == 0) return PAB_ERR_INVALID;
+    const RowPerm perm{n_b, n_t, n_s, h_layout == PAB_LAYOUT_A2A ? n_w : (h_layout == PAB_LAYOUT_TOKEN ? -1 : 0)};
+    return residual_modnorm_impl(x_in, x_out, pending, n_pending, gamma, beta, mod, h_out, n_b * n_t * n_s, D, eps,
+                                 mode, perm, tm, stream);
+}
+
 static int residual_modnorm_impl(const float* x_in, float* x_out, const void* const* pending,
                                  int n_pending, const float* gamma, const float* beta,
                                  const float* mod, void* h_out, int64_t rows, int D, float eps,
@@ -404,8 +432,11 @@ static int residual_modnorm_impl(const float* x_in, float* x_out, const void* co
     if (mode == 0 && !write_x) return PAB_OK;
     PendingList pl = make_pending(pending, n_pending);
     pl.tm_mask = tm.mask;
+    pl.a2a_mask = tm.a2a;
     pl.tm_t = tm.t;
     pl.tm_s = tm.s;
+    pl.n_b = tm.n_b;
+    pl.n_w = tm.n_w;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     auto* h = reinterpret_cast<__nv_bfloat16*>(h_out);
     bool aligned = (D % 4 == 0) && ((uintptr_t)x_in % 16 == 0) && ((uintptr_t)x_out % 16 == 0) &&

@@ -31,18 +31,29 @@ def _need(t: torch.Tensor, dtype, name: str):
         raise ValidationError(f"{name} must be {dtype}, got {t.dtype}")
 
 
+LAYOUT_FRAME, LAYOUT_TOKEN, LAYOUT_A2A = 0, 1, 2
+
+
 def is_token_major(t) -> bool:
     """Site outputs of the serial temporal site are stored token-major (rows (b, s, t))."""
     return bool(getattr(t, "pab_token_major", False))
 
 
+def term_layout(t) -> int:
+    """Row layout of a pending residual term: frame-major, token-major (serial temporal
+    site) or all-to-all order (sequence-parallel temporal site, ``pab_a2a_world`` ranks)."""
+    if getattr(t, "pab_a2a_world", 0):
+        return LAYOUT_A2A
+    return LAYOUT_TOKEN if is_token_major(t) else LAYOUT_FRAME
+
+
 def residual_modnorm(x_in, x_out, pending, h_out=None, mod=None, gamma=None, beta=None, mode=1, eps=1e-5,
-                     shape=None, h_token_major=False):
+                     shape=None, h_token_major=False, h_layout=None, n_w=1):
     """x_out = x_in + sum(pending) (fp32); h_out = modnorm(x_out) (mode 1) or bf16(x_out) (mode 2).
 
-    ``shape`` = (B, T, S) of the residual stream; needed when a pending term is
-    token-major (``is_token_major``) or when ``h_token_major`` asks for h in
-    (b, s, t) row order (the temporal site's input layout).
+    ``shape`` = (B, T, S) of the residual stream (block); needed when a pending term is not
+    frame-major (``term_layout``) or when h is written token-major (``h_token_major``) or in
+    all-to-all send order over ``n_w`` ranks (``h_layout=LAYOUT_A2A``).
     """
     lib = _lib.load()
     _need(x_in, torch.float32, "x_in")
@@ -59,22 +70,27 @@ def residual_modnorm(x_in, x_out, pending, h_out=None, mod=None, gamma=None, bet
         _need(h_out, torch.bfloat16, "h_out")
         if h_out.numel() != x_in.numel():
             raise ShapeError("h_out does not match the residual stream")
-    tm_needed = h_token_major or any(is_token_major(p) for p in pending)
-    if tm_needed:
-        if shape is None or shape[0] * shape[1] * shape[2] != rows:
-            raise ShapeError("token-major residual terms need the (B, T, S) shape of the stream")
-    pend = list(pending)
+    if h_layout is None:
+        h_layout = LAYOUT_TOKEN if h_token_major else LAYOUT_FRAME
+    layouts = [term_layout(p) for p in pending]
+    for p, lay in zip(pending, layouts):
+        if lay == LAYOUT_A2A:
+            n_w = int(p.pab_a2a_world)
+    general = h_layout != LAYOUT_FRAME or any(layouts)
+    if general and (shape is None or shape[0] * shape[1] * shape[2] != rows):
+        raise ShapeError("permuted residual terms / outputs need the (B, T, S) shape of the stream")
+    pend = list(zip(pending, layouts))
     src = x_in
 
-    def call(terms, h, m, md, tokmaj):
-        arr = _lib.ptr_array([p.data_ptr() for p in terms])
+    def call(terms, h, m, md, hl):
+        arr = _lib.ptr_array([p.data_ptr() for p, _ in terms])
         ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
-        if tm_needed:
-            mask = sum(1 << i for i, p in enumerate(terms) if is_token_major(p))
-            st = lib.pab_residual_modnorm_tm(src.data_ptr(), x_out.data_ptr(), arr, len(terms), mask, ptr(gamma),
-                                             ptr(beta), ptr(md), ptr(h), shape[0], shape[1], shape[2], D,
-                                             float(eps), int(m), int(tokmaj), _stream())
-            _lib.check(st, "pab_residual_modnorm_tm")
+        if general:
+            lay = (ctypes.c_int * max(1, len(terms)))(*[l for _, l in terms])
+            st = lib.pab_residual_modnorm_ex(src.data_ptr(), x_out.data_ptr(), arr, lay, len(terms), ptr(gamma),
+                                             ptr(beta), ptr(md), ptr(h), shape[0], shape[1], shape[2], int(n_w), D,
+                                             float(eps), int(m), int(hl), _stream())
+            _lib.check(st, "pab_residual_modnorm_ex")
         else:
             st = lib.pab_residual_modnorm(src.data_ptr(), x_out.data_ptr(), arr, len(terms), ptr(gamma), ptr(beta),
                                           ptr(md), ptr(h), rows, D, float(eps), int(m), _stream())
@@ -83,42 +99,22 @@ def residual_modnorm(x_in, x_out, pending, h_out=None, mod=None, gamma=None, bet
     # more than MAX_PENDING terms: drain in order, normalising only on the last chunk
     while len(pend) > MAX_PENDING:
         chunk, pend = pend[:MAX_PENDING], pend[MAX_PENDING:]
-        call(chunk, None, 0, None, False)
+        call(chunk, None, 0, None, LAYOUT_FRAME)
         src = x_out
-    call(pend, h_out, mode, mod, h_token_major)
+    call(pend, h_out, mode, mod, h_layout)
 
 
 def residual_modnorm_sp(x_in, x_out, pending, h_out, shard_shape, n_w, mod=None, gamma=None, beta=None, mode=1,
                         eps=1e-5):
     """residual_modnorm whose h output is written in all-to-all send order:
     shard rows (b, t, s) of shape (n_b, n_t, n_s) -> (dest, t, b, s_local)."""
-    lib = _lib.load()
     n_b, n_t, n_s, D = shard_shape
-    _need(x_in, torch.float32, "x_in")
-    _need(x_out, torch.float32, "x_out")
-    _need(h_out, torch.bfloat16, "h_out")
     if x_in.numel() != n_b * n_t * n_s * D or h_out.numel() != x_in.numel():
         raise ShapeError("sequence-parallel prologue buffers do not match the shard shape")
-    pend = list(pending)
-    src = x_in
-    while len(pend) > MAX_PENDING:
-        residual_modnorm(src, x_out, pend[:MAX_PENDING], mode=0)
-        pend, src = pend[MAX_PENDING:], x_out
-    for p in pend:
-        _need(p, torch.bfloat16, "pending term")
-        if p.numel() != x_in.numel():
-            raise ShapeError("pending term does not match the residual shard")
-    arr = _lib.ptr_array([p.data_ptr() for p in pend])
-    _lib.check(
-        lib.pab_residual_modnorm_sp(
-            src.data_ptr(), x_out.data_ptr(), arr, len(pend),
-            gamma.data_ptr() if gamma is not None else None,
-            beta.data_ptr() if beta is not None else None,
-            mod.data_ptr() if mod is not None else None, h_out.data_ptr(),
-            n_b, n_t, n_s, n_w, D, float(eps), int(mode), _stream(),
-        ),
-        "pab_residual_modnorm_sp",
-    )
+    if mode == 0:
+        raise ValidationError("the all-to-all ordered prologue needs an h output (mode 1 or 2)")
+    residual_modnorm(x_in, x_out, pending, h_out=h_out, mod=mod, gamma=gamma, beta=beta, mode=mode, eps=eps,
+                     shape=(n_b, n_t, n_s), h_layout=LAYOUT_A2A, n_w=n_w)
 
 
 def ddim_cfg(z, r, pending, guidance: bool, guidance_scale: float, a_cur: float, a_next: float):
@@ -128,7 +124,7 @@ def ddim_cfg(z, r, pending, guidance: bool, guidance_scale: float, a_cur: float,
     batch = z.shape[0]
     n = z.numel() // batch
     pend = list(pending)
-    if any(is_token_major(p) for p in pend) or len(pend) > MAX_PENDING:
+    if any(term_layout(p) for p in pend) or len(pend) > MAX_PENDING:
         raise ShapeError("ddim_cfg takes at most MAX_PENDING frame-major terms; flush the rest first")
     arr = _lib.ptr_array([p.data_ptr() for p in pend])
     _lib.check(

@@ -40,7 +40,7 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from .diffusion import DEFAULT_NOISE, NoiseParams, default_text_ids, initial_latent
+from .diffusion import DEFAULT_NOISE, GraphReplay, NoiseParams, default_text_ids, initial_latent
 from .errors import PolicyError, ShapeError, ValidationError
 from .model import ComponentKind, ModelParams
 from .policies import CacheStore, DecisionTable, PabPolicy, PolicyConfig, build_schedule
@@ -351,6 +351,7 @@ class _SPTemporal:
         self.attn_tok = torch.empty((rows_tok, D), **bf)
         self.o_tok = torch.empty((T, B, Sw, D), **bf)
         self.o_recv = torch.empty((world, Tl, B, Sw, D), **bf)
+        self.o_recv.pab_a2a_world = world
         q, k, v = self.qkv_tok[:, :D], self.qkv_tok[:, D:2 * D], self.qkv_tok[:, 2 * D:]
         ld = 3 * D
         # token layout rows (t, b, s): problem (a = b, b_idx = s), rows i = t (stride B*Sw rows)
@@ -384,10 +385,13 @@ class _SPTemporal:
             kernels.gemm(self.h_tok.view(-1, ctx.D), p.w_qkv_t, self.qkv_tok)
             kernels.attention(self.args, ctx.attn_impl)
             kernels.gemm(self.attn_tok, p.wo_t, self.o_tok.view(-1, ctx.D))
-            exchange_tokens_to_frames(self.o_tok, self.o_recv, self.group)
+            # the received output stays in all-to-all order (W_src, T/W, B, S/W, D); the next
+            # prologue adds it through its row map (PAB_LAYOUT_A2A) -- no unpack pass.  A cached
+            # output is received straight into its own buffer.
+            o = torch.empty_like(self.o_recv) if store else self.o_recv
+            exchange_tokens_to_frames(self.o_tok, o, self.group)
             self._log(st.step, li)
-            o = st.out_buffer(store)
-            unpack_frames(self.o_recv, o.view(ctx.B, ctx.T, ctx.S, ctx.D))
+            o.pab_a2a_world = self.W
             if store:
                 st.cache.store(site, o, st.step, "outputs")
             ctx.launches.attention_calls += 1
@@ -410,8 +414,9 @@ class _SPTemporal:
                                                  self.el > 0, self.wire))
 
 
-class ShardedDenoiser:
-    """Frame-sharded denoising run on this rank (broadcast SP)."""
+class ShardedDenoiser(GraphReplay):
+    """Frame-sharded denoising run on this rank (broadcast SP).  With an NCCL group the
+    whole video -- all-to-alls included -- replays as one CUDA graph (``capture_graph``)."""
 
     def __init__(self, params: ModelParams, schedule, table: DecisionTable, text_ids, *, guidance: bool,
                  guidance_scale: float, rank: int, world: int, group=None, method: str = "broadcast_sp",
@@ -506,7 +511,10 @@ class ShardedDenoiser:
         # caller's (pinned) buffer, no host-side gather of the strided frame slice
         for j, b in enumerate(bs):
             z[j].copy_(x_host[b, sl], non_blocking=True)
-        self.run(z)
+        if getattr(self, "_graph", None) is not None:
+            self.run_graph(z)
+        else:
+            self.run(z)
         if out is None:
             return z.cpu()
         for j, b in enumerate(bs):
@@ -560,11 +568,12 @@ class ParallelRunResult:
 
         for site, entry in sorted(local.entries.items(), key=lambda kv: str(kv[0])):
             # a rank group of one runs the serial temporal site, whose cache is token-major
-            v = canonical(entry.value, (self._batch, self.plan.frames_per_worker, self._tail[0])).contiguous()
+            shard = (self._batch, self.plan.frames_per_worker, self._tail[0])
+            v = canonical(entry.value, shard).contiguous()
             if multi:
                 parts = _all_gather(v.contiguous())
             else:
-                parts = [c.entries[site].value for c in self.worker_caches]
+                parts = [canonical(c.entries[site].value, shard) for c in self.worker_caches]
             B = self._batch
             parts = [p.reshape(B, -1, *self._tail) for p in parts]
             gw = getattr(self, "_split_gw", None)

@@ -548,7 +548,7 @@ def run_forward(ctx: StepContext, step_index: int, t: float, z, r, decisions, ca
     else:
         guidance, g, a_cur, a_next = ddim
         if st.src is not st.r or len(st.pending) > kernels.MAX_PENDING or any(
-                kernels.is_token_major(p) for p in st.pending):
+                kernels.term_layout(p) for p in st.pending):
             st.flush()  # the fused DDIM kernel drains frame-major terms only
         kernels.ddim_cfg(z, st.r, st.pending, guidance, g, a_cur, a_next)
         ctx.launches.other_calls += 1
@@ -557,10 +557,15 @@ def run_forward(ctx: StepContext, step_index: int, t: float, z, r, decisions, ca
 
 def canonical(o, shape):
     """Frame-major (B, T, S, D) view of a site output (token-major outputs of the
-    serial temporal site are permuted back); for tests and gathered caches."""
+    serial temporal site and all-to-all ordered outputs of the sequence-parallel one
+    are permuted back); for tests and gathered caches."""
     B, T, S = shape
-    if kernels.is_token_major(o):
+    lay = kernels.term_layout(o)
+    if lay == kernels.LAYOUT_TOKEN:
         return o.view(B, S, T, -1).permute(0, 2, 1, 3).reshape(B, T, S, -1)
+    if lay == kernels.LAYOUT_A2A:
+        W = int(o.pab_a2a_world)
+        return o.view(W, T, B, S // W, -1).permute(2, 1, 0, 3, 4).reshape(B, T, S, -1)
     return o.view(B, T, S, -1)
 
 

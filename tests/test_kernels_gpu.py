@@ -251,3 +251,30 @@ def test_fill_uniform_matches_host_stream():
     dst16 = torch.zeros(rows, cols, device=DEV, dtype=torch.bfloat16)
     kernels.fill_uniform(dst16, rows, cols, 0, seed, 1000, -0.25, 0.25)
     assert torch.equal(dst16, torch.from_numpy(want).to(DEV).to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("W,mode", [(2, 1), (4, 2), (8, 0)])
+def test_residual_modnorm_all_to_all_order_terms(W, mode):
+    """PAB_LAYOUT_A2A pending terms (the sequence-parallel temporal site's received output,
+    (W_src, T/W, B, S/W, D)) are added through the prologue's row map, equal to unpacking
+    them first (reference parallel.reshard, parallel.py:140-180)."""
+    B, Tl, S, D = 2, 4, 96, 144
+    rows = B * Tl * S
+    g = torch.Generator(device=DEV).manual_seed(W)
+    x = torch.randn(rows, D, device=DEV, generator=g)
+    recv = torch.randn(W, Tl, B, S // W, D, device=DEV, generator=g).to(torch.bfloat16)
+    recv.pab_a2a_world = W
+    plain = torch.randn(rows, D, device=DEV, generator=g).to(torch.bfloat16)
+    mod = torch.randn(2 * D, device=DEV, generator=g) * 0.1
+    x_out = torch.empty_like(x)
+    h = torch.empty(rows, D, device=DEV, dtype=torch.bfloat16)
+    kernels.residual_modnorm(x, x_out, [plain, recv], h_out=h if mode else None, mod=mod, mode=mode,
+                             shape=(B, Tl, S))
+    unpacked = recv.permute(2, 1, 0, 3, 4).reshape(rows, D)
+    want = x + plain.float() + unpacked.float()
+    assert torch.equal(x_out, want)
+    if mode == 1:
+        ln = torch.nn.functional.layer_norm(want, (D,), eps=1e-5)
+        check_close(h, ln * (1.0 + mod[D:]) + mod[:D], "modnorm a2a", 6e-3)
+    elif mode == 2:
+        assert torch.equal(h, want.to(torch.bfloat16))

@@ -139,3 +139,72 @@ def test_logical_workers_without_process_group(world, guidance, split):
                               split_batch=split)
     assert par.comm_report.grouped_elements() == model.grouped_elements()
     assert len(par.worker_caches) == world and len(par.gathered_cache()) > 0
+
+
+def _nccl_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        from oracle import pab_oracle as orc
+        from paper_2408_12588_b200.diffusion import initial_latent, make_schedule
+        from paper_2408_12588_b200.model import ModelConfig, init_model
+        from paper_2408_12588_b200.parallel import ShardedDenoiser, run_parallel
+        from paper_2408_12588_b200.policies import PabPolicy, build_schedule
+
+        cfg = ModelConfig(layers=2, hidden=144, heads=2, frames=8, spatial_tokens=64, text_tokens=12,
+                          cross_in_temporal=True)
+        params = init_model(cfg, seed=3)
+        sched = make_schedule(8)
+        pol = PabPolicy(2, 3, 2, window=(990.0, 10.0))
+        table = build_schedule(pol, sched, cfg.layers)
+        par = run_parallel(params, sched, pol, world, "broadcast_sp", seed=7, guidance=True, table=table)
+        # the same run replayed as one CUDA graph with the NCCL all-to-alls captured inside
+        den = ShardedDenoiser(params, sched, table, np.arange(12), guidance=True, guidance_scale=4.0, rank=rank,
+                              world=world)
+        x = torch.from_numpy(initial_latent(params, 7, 2)).cuda()
+        z = den.shard_input(x)
+        den.capture_graph()
+        den.run_graph(z)
+        parts = [torch.empty_like(z) for _ in range(world)]
+        dist.all_gather(parts, z)
+        graph_latent = torch.cat(parts, dim=1).cpu().numpy()
+        out = {"rank": rank}
+        if rank == 0:
+            ocfg = orc.Cfg(2, 144, 2, 8, 64, 12, cross_in_temporal=True)
+            want = orc.sample(ocfg, orc.init_weights(ocfg, 3), orc.linear_timesteps(8), table.source, seed=7,
+                              text_ids=np.arange(12), guidance=True)
+            out["rel"] = float(np.linalg.norm(par.latent.astype(np.float64) - want) / np.linalg.norm(want))
+            out["max"] = float(np.abs(par.latent - want).max() / np.abs(want).max())
+            out["graph_equal"] = bool(np.array_equal(graph_latent, par.latent))
+        q.put(out)
+    except Exception as e:  # surface worker failures to the test
+        q.put({"rank": rank, "error": repr(e)})
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="NCCL broadcast SP needs >= 2 GPUs (the gpurun box has one)")
+def test_nccl_broadcast_sp_vs_oracle_and_graph():
+    """Broadcast SP over NCCL on real GPUs (one process per GPU): latents vs the CPU oracle's
+    serial run within the CFG gate, and a CUDA-graph replay with the all-to-alls captured
+    equal to the eager run bit for bit."""
+    from gates import MAX_TOL_CFG, REL_TOL_CFG
+
+    world = min(torch.cuda.device_count(), 8)
+    world = 1 << (world.bit_length() - 1)  # W | T = 8
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_nccl_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    errs = [r for r in res if "error" in r]
+    assert not errs, errs
+    r0 = [r for r in res if r["rank"] == 0][0]
+    assert r0["rel"] <= REL_TOL_CFG and r0["max"] <= MAX_TOL_CFG, r0
+    assert r0["graph_equal"], r0
