@@ -18,6 +18,8 @@ bool attn_tc_supported(const pab_attn_args* a);                 // attn_tc.cu
 int attn_tc_packing(const pab_attn_args* a);                    // attn_tc.cu: >0 = packed short sequences
 int attn_fa_launch(const pab_attn_args* a, cudaStream_t st);  // attn_fa.cu
 bool attn_fa_supported(const pab_attn_args* a);                // attn_fa.cu
+int attn_tm_launch(const pab_attn_args* a, cudaStream_t st);  // attn_tm.cu
+bool attn_tm_supported(const pab_attn_args* a);                // attn_tm.cu
 
 namespace {
 
@@ -125,8 +127,10 @@ extern "C" int pab_attention(const pab_attn_args* a, int impl, void* stream) {
     if (impl == 0) impl = 1;
     if (impl == 1) {
         // long sequences: row-per-thread kernel (attn_fa.cu); short packed sequences
-        // (temporal attention): block-diagonal kernel (attn_tc.cu)
+        // (temporal attention): diagonal-window kernel (attn_tm.cu) when T divides 32, else
+        // the block-diagonal kernel (attn_tc.cu)
         if (!attn_tc_supported(a)) return PAB_ERR_UNSUPPORTED;
+        if (attn_tc_packing(a) && attn_tm_supported(a)) return attn_tm_launch(a, st);
         return (attn_tc_packing(a) || !attn_fa_supported(a)) ? attn_tc_launch(a, st) : attn_fa_launch(a, st);
     }
     if (impl == 2) return attn_simt_launch(a, st);
