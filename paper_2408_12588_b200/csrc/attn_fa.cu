@@ -75,6 +75,11 @@ constexpr uint32_t kSCol = 0, kPCol = 384;
 #define PAB_FA_SINGLES_LAST 1  // single-tile items (odd tile count) scheduled last
 #endif
 
+#ifndef PAB_FA_PV_SPLIT
+#define PAB_FA_PV_SPLIT 1  // 1: P.V issued per query tile (own p_full / o_done), 0: one group for both
+#endif
+constexpr bool kPvSplit = PAB_FA_PV_SPLIT != 0;
+
 #ifndef PAB_FA_POLY_DIV
 #define PAB_FA_POLY_DIV 3   // one column pair in PAB_FA_POLY_DIV on the FMA pipe (0: MUFU only)
 #endif
@@ -133,7 +138,8 @@ struct Geometry {
 struct Bars {
     uint64_t q_full[2], q_empty[2], k_full[3], k_empty[3], v_full[3], v_ready[3], v_empty[3];
     uint64_t q_ready[2], k_ready[3];  // Q / K tiles after the fixer warp's pad-column patch
-    uint64_t s_full, s_free, p_full, o_done;  // shared by the two query tiles (they run in phase)
+    uint64_t s_full, s_free;         // shared by the two query tiles (S is one interleaved MMA group)
+    uint64_t p_full[2], o_done[2];   // per tile (PAB_FA_PV_SPLIT) or index 0 for both
 };
 
 // single-thread tcgen05.mma issue (lane 0 of the MMA warp): descriptors are passed as
@@ -391,8 +397,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_init(&bars->s_full, 1);
         mbar_init(&bars->s_free, kSoftmaxWarps);  // one arrival per softmax warp
-        mbar_init(&bars->p_full, kSoftmaxWarps);
-        mbar_init(&bars->o_done, 1);
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(&bars->p_full[t], kPvSplit ? kSoftmaxWarps / 2 : kSoftmaxWarps);
+            mbar_init(&bars->o_done[t], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == kMmaWarp) {
@@ -412,6 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // warp = 8 t + 4 h + quarter: TMEM lane quarter = warp % 4 (the tcgen05.ld/st lane
         // restriction), column half h of the 112-key S tile
         const int t = warp / (4 * kSplit);
+        const int tb = kPvSplit ? t : 0;  // this tile's p_full / o_done barrier
         const int hc = (warp >> 2) % kSplit;
         const int wl = warp & 3;
         const int row = wl * 32 + lane;
@@ -520,9 +529,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&bars->s_free);
                     if (PAB_FA_LAG && kSplit == 1) asm volatile("bar.sync %0, 64;" ::"r"(3 + wl + 4 * (it_n & 1)) : "memory");
-                    if (it_n > 0) mbar_wait(&bars->o_done, (it_n - 1) & 1);
+                    if (it_n > 0) mbar_wait(&bars->o_done[tb], (it_n - 1) & 1);
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&bars->p_full);
+                    if (lane == 0) mbar_arrive(&bars->p_full[tb]);
                     continue;
                 }
                 if (kSplit == 1) {
@@ -544,9 +553,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool masked = !padmask && (j == n_kv - 1) && (tail < kHalf);
                 // lag token (warps wl of tile 0 and tile 1 share an SM sub-partition): tile 1 starts
                 // its ALU-bound row max only when tile 0's is done, so it overlaps tile 0's MUFU-bound
-                // exp; the shared s_free / p_full barriers absorb a lag of one phase.  Two named
-                // barriers alternate by iteration parity: tile 0 can reach iteration j + 1's token
-                // before tile 1 consumed j's, never j + 2's (that P store needs tile 1's p_full(j)).
+                // exp.  Two named barriers alternate by iteration parity: tile 0 can reach iteration
+                // j + 1's token before tile 1 consumed j's, never j + 2's (S(j + 2) is issued only
+                // after the shared s_free(j + 1), i.e. after tile 1 loaded S(j + 1), which follows
+                // its token of iteration j).
                 // Barrier ids 3..10 (1 and 2 are the epilogue's per-tile barriers).
                 if (PAB_FA_LAG == 1 && kSplit == 1 && t == 1) asm volatile("bar.sync %0, 64;" ::"r"(3 + wl + 4 * (it_n & 1)) : "memory");
                 if (masked) {
@@ -579,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (__any_sync(0xffffffffu, need)) {
                     const float m_new = need ? m_tile : m_run;
                     if (j > 0) {
-                        mbar_wait(&bars->o_done, (it_n - 1) & 1);
+                        mbar_wait(&bars->o_done[tb], (it_n - 1) & 1);
                         tc_fence_after();
                         waited = true;
                         const float alpha = fast_exp2(m_run - m_new);
@@ -624,7 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (PAB_FA_LAG == 2 && kSplit == 1 && t == 0) asm volatile("bar.arrive %0, 64;" ::"r"(3 + wl + 4 * (it_n & 1)) : "memory");
                 FA_TRACE(trc, it_n, t, 4);
                 if (!waited && it_n > 0) {
-                    mbar_wait(&bars->o_done, (it_n - 1) & 1);
+                    mbar_wait(&bars->o_done[tb], (it_n - 1) & 1);
                     tc_fence_after();
                 }
                 if (j == 0 && have_prev) epilogue(prev);  // O of the previous item is final
@@ -641,7 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_wait_st();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->p_full);
+                if (lane == 0) mbar_arrive(&bars->p_full[tb]);
                 FA_TRACE(trc, it_n, t, 5);
             }
             if (active) {
@@ -650,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         if (have_prev) {
-            mbar_wait(&bars->o_done, (it_n - 1) & 1);
+            mbar_wait(&bars->o_done[tb], (it_n - 1) & 1);
             tc_fence_after();
             epilogue(prev);
         }
@@ -810,6 +820,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mma_ts1(tmem + G::kOCol0 + G::kOStride * t, tmem + kPCol + 64 * t + 8 * k,
                             (va + ((512 * k) >> 4)) | kLboV, kHi32, idO, accumulate | (k > 0));
         };
+        // O_t += P_t V for one tile (a single-accumulator chain of ncols / 16 K-steps)
+        auto issue_pv_tile = [&](int vst, int t, uint32_t accumulate, int ncols) {
+            const uint32_t va = v_lo + ((vst * G::kSlotKV) >> 4);
+            const uint32_t o_t = tmem + G::kOCol0 + G::kOStride * t, p_t = tmem + kPCol + 64 * t;
+            if (kKv / 16 == 7) {
+                const uint64_t dv = ((uint64_t)kHi32 << 32) | (va | kLboV);
+                mma_group_pv7(o_t, o_t, p_t, p_t, dv, idO, accumulate, 0, ncols / 16);
+                return;
+            }
+            if (lane != 0) return;
+            for (int k = 0; 16 * k < ncols; ++k)
+                mma_ts1(o_t, p_t + 8 * k, (va + ((512 * k) >> 4)) | kLboV, kHi32, idO, accumulate | (k > 0));
+        };
         // iteration gi = (item c, kv tile j), KV tile g.  The tiles run in phase: S(gi+1) of
         // both tiles is issued once both softmaxes have read S(gi) (early in their iteration),
         // PV(gi) once both have stored P(gi).
@@ -845,11 +868,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             // ---- PV of this iteration
             FA_TRACE(lane == 0, gi, 1, 10);
-            mbar_wait2(&bars->p_full, gi & 1, &bars->v_ready[g % 3], (g / 3) & 1);
-            tc_fence_after();
-            FA_TRACE(lane == 0, gi, 1, 8);
-            issue_pv(g % 3, j > 0, cols_of(j), it.two);
-            tc_commit(&bars->o_done);
+            if (kPvSplit) {
+                // tile 0's P.V goes as soon as tile 0's P is stored: its next P store (which
+                // must wait for this P.V) no longer waits behind tile 1's exp section
+                mbar_wait2(&bars->p_full[0], gi & 1, &bars->v_ready[g % 3], (g / 3) & 1);
+                tc_fence_after();
+                FA_TRACE(lane == 0, gi, 1, 8);
+                issue_pv_tile(g % 3, 0, j > 0, cols_of(j));
+                tc_commit(&bars->o_done[0]);
+                mbar_wait(&bars->p_full[1], gi & 1);
+                tc_fence_after();
+                if (it.two) issue_pv_tile(g % 3, 1, j > 0, cols_of(j));
+                tc_commit(&bars->o_done[1]);
+            } else {
+                mbar_wait2(&bars->p_full[0], gi & 1, &bars->v_ready[g % 3], (g / 3) & 1);
+                tc_fence_after();
+                FA_TRACE(lane == 0, gi, 1, 8);
+                issue_pv(g % 3, j > 0, cols_of(j), it.two);
+                tc_commit(&bars->o_done[0]);
+            }
             tc_commit(&bars->v_empty[g % 3]);
             FA_TRACE(lane == 0, gi, 1, 9);
             ++g;
