@@ -56,16 +56,21 @@ def launches(src, dst):
 def full(src, dst):
     raw = subprocess.run(["ncu", "-i", src, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    h = rows[0]
+    h, units = rows[0], rows[1]
+    # ncu scales units per value (Mbyte / Gbyte, us / ms): normalise bytes to MB, time to us
+    to_base = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "ns": 1e-3, "nsecond": 1e-3, "us": 1.0,
+               "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
     res = []
     for r in rows[2:]:
         d = {"kernel": r[h.index("Kernel Name")][:90]}
         for m in METRICS:
             if m in h:
+                i = h.index(m)
                 try:
-                    d[m] = float(r[h.index(m)].replace(",", ""))
+                    d[m] = float(r[i].replace(",", "")) * to_base.get(units[i], 1.0)
                 except ValueError:
-                    d[m] = r[h.index(m)]
+                    d[m] = r[i]
+        d["units"] = "bytes in MB, durations in us"
         res.append(d)
     json.dump(res, open(dst, "w"), indent=1)
     print(json.dumps(res, indent=1))
