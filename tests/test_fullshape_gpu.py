@@ -118,3 +118,41 @@ def test_c5_spatial_attention_3600_tokens():
     ref = ref.permute(0, 2, 1, 3).reshape(B * S, D)
     rel = float((out.float() - ref).norm() / ref.norm())
     assert rel < 1.2e-2, rel
+
+
+def test_c3_four_layers_thirty_steps_vs_oracle_fixture():
+    """C3 at full width and 4 of its 28 layers over the whole 30-step opensora-pab246
+    schedule (CFG g=4) against the CPU oracle's run stored in tests/golden/c3_deep.npz
+    (tests/golden/make_c3_deep.py): per-step latent norm, max|x| and a strided
+    8192-element subsample.  Broadcast reuse compounds over the 30 steps here, which
+    the one-layer slices above cannot show."""
+    import os
+
+    path = os.path.join(os.path.dirname(__file__), "golden", "c3_deep.npz")
+    if not os.path.exists(path):
+        pytest.skip("tests/golden/c3_deep.npz not generated (tests/golden/make_c3_deep.py)")
+    fx = np.load(path)
+    L, N = int(fx["layers"]), int(fx["steps"])
+    cfg = ModelConfig(layers=L, hidden=1152, heads=16, frames=16, spatial_tokens=1560, text_tokens=300,
+                      cross_in_temporal=True)
+    params = init_model(cfg, seed=11)
+    table = DecisionTable(fx["table"])
+    den = Denoiser(params, make_schedule(N), table, np.arange(300) % 256, guidance=True, guidance_scale=4.0)
+    z = torch.from_numpy(initial_latent(params, 11, 2)).cuda()
+    idx = torch.from_numpy(fx["idx"]).cuda()
+    got_sub, got_norm, got_max = [], [], []
+
+    def on_step(i, zz):
+        flat = zz.reshape(-1)
+        got_sub.append(flat[idx].cpu().numpy().astype(np.float64))
+        got_norm.append(float(flat.double().norm()))
+        got_max.append(float(flat.abs().max()))
+
+    den.run(z, on_step=on_step)
+    assert den.ctx.launches.sites_reused > 0
+    for i in range(N):
+        w = fx["sub"][i].astype(np.float64)
+        rel = np.linalg.norm(got_sub[i] - w) / np.linalg.norm(w)
+        mx = np.abs(got_sub[i] - w).max() / float(fx["maxabs"][i])
+        rn = abs(got_norm[i] - float(fx["norms"][i])) / float(fx["norms"][i])
+        assert rel < REL_TOL_CFG and mx < MAX_TOL_CFG and rn < REL_TOL_CFG, (i, rel, mx, rn)
