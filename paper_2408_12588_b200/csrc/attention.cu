@@ -20,8 +20,6 @@ int attn_fa_launch(const pab_attn_args* a, cudaStream_t st);  // attn_fa.cu
 bool attn_fa_supported(const pab_attn_args* a);                // attn_fa.cu
 int attn_tm_launch(const pab_attn_args* a, cudaStream_t st);  // attn_tm.cu
 bool attn_tm_supported(const pab_attn_args* a);                // attn_tm.cu
-int attn_f3_launch(const pab_attn_args* a, cudaStream_t st);  // attn_f3.cu
-bool attn_f3_supported(const pab_attn_args* a);                // attn_f3.cu
 
 namespace {
 
@@ -136,9 +134,5 @@ extern "C" int pab_attention(const pab_attn_args* a, int impl, void* stream) {
         return (attn_tc_packing(a) || !attn_fa_supported(a)) ? attn_tc_launch(a, st) : attn_fa_launch(a, st);
     }
     if (impl == 2) return attn_simt_launch(a, st);
-    if (impl == 3) {  // three-tile long-sequence kernel (A/B against impl 1)
-        if (!attn_tc_supported(a) || attn_tc_packing(a) || !attn_f3_supported(a)) return PAB_ERR_UNSUPPORTED;
-        return attn_f3_launch(a, st);
-    }
     return PAB_ERR_INVALID;
 }
