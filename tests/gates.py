@@ -9,8 +9,8 @@ fp32 oracle by (scripts/bf16_floor.py, worst step, relL2 / max|d|/max|ref|):
     dh72   L2 D288 T4 S128     -                     1.57e-2 / 1.75e-2
     C1     L4 D144 T8 S1024    4.6e-3 / 5.5e-3       -
     C2 slice L1 full width     -                     1.24e-2 / 1.77e-2
-    C3 slice L1 full width     -                     see DESIGN.md section 4
-    C4 slice L1 full width     -                     see DESIGN.md section 4
+    C3 slice L1 full width     -                     1.22e-2 / 1.77e-2
+    C4 slice L1 full width     -                     1.22e-2 / 1.79e-2
 
 CFG amplifies the eps rounding (eps_u + 4 (eps_c - eps_u)), hence the guided
 floor.  Guided runs are held to 1.5x the worst measured guided floor; unguided
