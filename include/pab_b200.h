@@ -30,6 +30,7 @@ extern "C" {
 #define PAB_ERR_UNSUPPORTED 5 /* shape outside what a kernel supports */
 
 #define PAB_MAX_PENDING 8     /* pending residual terms per launch */
+#define PAB_MAX_PEERS 8       /* ranks of a sequence-parallel group on one NVSwitch box */
 
 /* Library metadata. */
 const char* pab_version(void);
@@ -109,6 +110,47 @@ int pab_residual_modnorm_ex(const float* x_in, float* x_out,
                             const float* mod, void* h_out,
                             int64_t n_b, int64_t n_t, int64_t n_s, int64_t n_w,
                             int D, float eps, int mode, int h_layout, void* stream);
+
+/*
+ * Broadcast SP over NVLink peer memory (no collective): the frames->tokens and
+ * tokens->frames exchanges of the temporal site (reference parallel.reshard,
+ * pkg/src/pab_engine/parallel.py:140-180, 322-348) fused into the prologues.
+ *
+ *   h_layout == PAB_LAYOUT_PEER: h row (b, t, s) of this rank's frame shard is
+ *     stored straight into rank dst = s / (n_s/n_w)'s token-layout buffer
+ *     peer_h[dst] (T, n_b, n_s/n_w, D) at row ((rank * n_t + t) * n_b + b) *
+ *     (n_s/n_w) + s % (n_s/n_w)   -- the prologue's stores ARE the all-to-all.
+ *   term_layout[i] == PAB_LAYOUT_PEER: pending term i is read straight out of the
+ *     ranks' token-layout buffers peer_src[0..n_w) with the inverse map (the
+ *     temporal site's output, no return all-to-all and no unpack pass); at most
+ *     one such term per launch.  peer_copy != NULL: that term is also written
+ *     frame-major (n_b, n_t, n_s, D) into peer_copy (the broadcast cache slot, so
+ *     a later broadcast step reads it locally and communicates nothing).
+ * Every pointer must be mapped into this process (CUDA IPC / same process).
+ * Otherwise identical to pab_residual_modnorm_ex.  n_w <= PAB_MAX_PEERS.
+ */
+#define PAB_LAYOUT_PEER 3
+int pab_residual_modnorm_peer(const float* x_in, float* x_out,
+                              const void* const* pending, const int* term_layout, int n_pending,
+                              const void* const* peer_src, void* peer_copy,
+                              const float* gamma, const float* beta,
+                              const float* mod, void* h_out, void* const* peer_h,
+                              int64_t n_b, int64_t n_t, int64_t n_s, int64_t n_w, int rank,
+                              int D, float eps, int mode, int h_layout, void* stream);
+
+/*
+ * Device barrier of an n_w-rank group over peer memory (orders the peer stores
+ * and loads above; no reference counterpart -- the reference exchanges arrays in
+ * one process).  flags[q] = rank q's n_w-entry uint32 flag array (zeroed once,
+ * mapped here); counter = this rank's uint32 epoch counter (zeroed once).  The
+ * launch bumps the epoch, release-stores it into slot [rank] of every rank's
+ * flags and waits (acquire) until every slot of its own array reached it.
+ * Graph-capturable (the epoch lives on the device).  A wait longer than
+ * timeout_s stores PAB_PEER_TIMEOUT into *error and returns (never hangs).
+ */
+#define PAB_PEER_TIMEOUT 0x7ee1u
+int pab_peer_barrier(void* const* flags, void* counter, int rank, int n_w, void* error,
+                     double timeout_s, void* stream);
 
 /*
  * Fused end-of-step residual drain + classifier-free guidance + DDIM (K8).

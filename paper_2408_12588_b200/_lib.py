@@ -61,6 +61,14 @@ SIGNATURES = {
         [c_vp, c_vp, ctypes.POINTER(c_vp), c_vp, ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64,
          ctypes.c_int, ctypes.c_float, ctypes.c_int, ctypes.c_int, c_vp],
     ),
+    "pab_residual_modnorm_peer": (
+        ctypes.c_int,
+        [c_vp, c_vp, ctypes.POINTER(c_vp), c_vp, ctypes.c_int, ctypes.POINTER(c_vp), c_vp, c_vp, c_vp, c_vp, c_vp,
+         ctypes.POINTER(c_vp), c_i64, c_i64, c_i64, c_i64, ctypes.c_int, ctypes.c_int, ctypes.c_float, ctypes.c_int,
+         ctypes.c_int, c_vp],
+    ),
+    "pab_peer_barrier": (ctypes.c_int, [ctypes.POINTER(c_vp), c_vp, ctypes.c_int, ctypes.c_int, c_vp, ctypes.c_double,
+                                        c_vp]),
     "pab_ddim_cfg": (
         ctypes.c_int,
         [c_vp, c_vp, ctypes.POINTER(c_vp), ctypes.c_int, ctypes.c_int, c_i64, ctypes.c_int, ctypes.c_double,

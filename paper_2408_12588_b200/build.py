@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpab_b200.so")
 OBJ_DIR = os.path.join(HERE, "_build")
-SOURCES = ["capi.cu", "elementwise.cu", "attention.cu", "attn_tc.cu", "attn_fa.cu", "attn_tm.cu", "gemm.cu"]
+SOURCES = ["capi.cu", "elementwise.cu", "attention.cu", "attn_tc.cu", "attn_fa.cu", "attn_tm.cu", "gemm.cu", "peer.cu"]
 HEADERS = ["common.cuh", "tc_ptx.cuh", os.path.join("..", "..", "include", "pab_b200.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

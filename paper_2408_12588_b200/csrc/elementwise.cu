@@ -33,6 +33,9 @@ struct VecT<4> {
         float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
         v[0] += fa.x; v[1] += fa.y; v[2] += fb.x; v[3] += fb.y;
     }
+    __device__ static void copy_bf16(const __nv_bfloat16* src, __nv_bfloat16* dst) {
+        *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(src);
+    }
     __device__ static void store_bf16(__nv_bfloat16* p, const float* v) {
         __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]);
         __nv_bfloat162 b = __floats2bfloat162_rn(v[2], v[3]);
@@ -48,14 +51,20 @@ struct VecT<1> {
     __device__ static void store_f32(float* p, const float* v) { *p = v[0]; }
     __device__ static void add_bf16(const __nv_bfloat16* p, float* v) { v[0] += __bfloat162float(*p); }
     __device__ static void store_bf16(__nv_bfloat16* p, const float* v) { *p = __float2bfloat16_rn(v[0]); }
+    __device__ static void copy_bf16(const __nv_bfloat16* src, __nv_bfloat16* dst) { *dst = *src; }
 };
 
 // Optional row permutation of the h output: rows (b, t, s) of a frame-sharded
 // (n_b, n_t, n_s) block are written in all-to-all send order
 // (dest = s / (n_s / n_w), t, b, s % (n_s / n_w)) so the sequence-parallel
-// frames->tokens exchange needs no pack pass.  n_w == 0: identity.
+// frames->tokens exchange needs no pack pass.  n_w == 0: identity.  With peer[]
+// set (PAB_LAYOUT_PEER), the row goes straight into rank dest's token-layout
+// receive buffer (T, B, S/W, D) at ((me * n_t + t) * n_b + b) * (n_s / n_w) + s % (n_s / n_w):
+// the prologue's stores ARE the all-to-all, over NVLink peer memory.
 struct RowPerm {
     int64_t n_b, n_t, n_s, n_w;  // n_w > 0: all-to-all send order; n_w == -1: token-major (b, s, t)
+    int64_t me;                   // this rank (peer mode)
+    __nv_bfloat16* peer[PAB_MAX_PEERS];  // peer[0] != nullptr: destination buffers of the W ranks
     __device__ __forceinline__ int64_t map(int64_t row) const {
         if (n_w == 0) return row;
         if (n_w < 0) {
@@ -65,6 +74,14 @@ struct RowPerm {
         const int64_t s = row % n_s, bt = row / n_s, t = bt % n_t, b = bt / n_t;
         const int64_t sw = n_s / n_w, dst = s / sw, sl = s - dst * sw;
         return ((dst * n_t + t) * n_b + b) * sw + sl;
+    }
+    __device__ __forceinline__ __nv_bfloat16* out_row(__nv_bfloat16* h, int64_t row, int64_t D) const {
+        if (n_w > 0 && peer[0] != nullptr) {
+            const int64_t s = row % n_s, bt = row / n_s, t = bt % n_t, b = bt / n_t;
+            const int64_t sw = n_s / n_w, dst = s / sw, sl = s - dst * sw;
+            return peer[dst] + (((me * n_t + t) * n_b + b) * sw + sl) * D;
+        }
+        return h + map(row) * D;
     }
 };
 
@@ -78,7 +95,6 @@ __global__ void __launch_bounds__(256) residual_modnorm_kernel(
     const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (row >= rows) return;
     const int64_t base = row * (int64_t)D;
-    const int64_t hbase = perm.map(row) * (int64_t)D;
     float v[NV][VEC];
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
@@ -87,16 +103,21 @@ __global__ void __launch_bounds__(256) residual_modnorm_kernel(
             VecT<VEC>::load_f32(x_in + base + c, v[j]);
 #pragma unroll
             for (int p = 0; p < PAB_MAX_PENDING; ++p)
-                if (p < pend.n) VecT<VEC>::add_bf16(pend.p[p] + pend.src_row(p, row) * (int64_t)D + c, v[j]);
+                if (p < pend.n) {
+                    const __nv_bfloat16* src = pend.row_ptr(p, row, D) + c;
+                    VecT<VEC>::add_bf16(src, v[j]);
+                    if (p == pend.copy_term) VecT<VEC>::copy_bf16(src, pend.copy + base + c);
+                }
             if (write_x) VecT<VEC>::store_f32(x_out + base + c, v[j]);
         }
     }
     if (mode == 0) return;
+    __nv_bfloat16* hrow = perm.out_row(h_out, row, D);
     if (mode == 2) {
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
             const int c = (j * 32 + lane) * VEC;
-            if (c < D) VecT<VEC>::store_bf16(h_out + hbase + c, v[j]);
+            if (c < D) VecT<VEC>::store_bf16(hrow + c, v[j]);
         }
         return;
     }
@@ -135,7 +156,7 @@ __global__ void __launch_bounds__(256) residual_modnorm_kernel(
                 if (gamma) h = h * gamma[c + e] + beta[c + e];
                 o[e] = h * (1.0f + mod[D + c + e]) + mod[c + e];
             }
-            VecT<VEC>::store_bf16(h_out + hbase + c, o);
+            VecT<VEC>::store_bf16(hrow + c, o);
         }
     }
 }
@@ -161,9 +182,13 @@ __global__ void __launch_bounds__(256) residual_modnorm_exact_kernel(
     for (int p = 0; p < PAB_MAX_PENDING; ++p) {
         if (p < pend.n) {
             uint2 raw[NV];
+            const uint2* src = reinterpret_cast<const uint2*>(pend.row_ptr(p, row, D));
 #pragma unroll
-            for (int j = 0; j < NV; ++j)
-                raw[j] = __ldcs(reinterpret_cast<const uint2*>(pend.p[p] + pend.src_row(p, row) * (int64_t)D) + j * 32 + lane);
+            for (int j = 0; j < NV; ++j) raw[j] = __ldcs(src + j * 32 + lane);
+            if (p == pend.copy_term) {
+#pragma unroll
+                for (int j = 0; j < NV; ++j) __stcs(reinterpret_cast<uint2*>(pend.copy + base) + j * 32 + lane, raw[j]);
+            }
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
                 const float2 a = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&raw[j].x));
@@ -177,7 +202,7 @@ __global__ void __launch_bounds__(256) residual_modnorm_exact_kernel(
         for (int j = 0; j < NV; ++j) __stcs(reinterpret_cast<float4*>(x_out + base) + j * 32 + lane, v[j]);
     }
     if (mode == 0) return;
-    __nv_bfloat16* hrow = h_out + perm.map(row) * (int64_t)D;
+    __nv_bfloat16* hrow = perm.out_row(h_out, row, D);
     auto store_h = [&](int j, float a, float b, float c, float d) {
         __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
         uint2 raw;
@@ -354,6 +379,10 @@ struct TmState {
     int64_t t, s;
     uint32_t a2a = 0;
     int64_t n_b = 1, n_w = 1;
+    uint32_t peer = 0;                    // bit i: term i is PAB_LAYOUT_PEER
+    int64_t me = 0;                       // this rank (peer terms / peer h output)
+    const void* const* peer_src = nullptr;  // n_w token-layout source buffers of the PEER term
+    void* copy = nullptr;                 // frame-major copy of the PEER term (cache slot) or NULL
 };
 static int residual_modnorm_impl(const float* x_in, float* x_out, const void* const* pending,
                                  int n_pending, const float* gamma, const float* beta,
@@ -391,29 +420,71 @@ extern "C" int pab_residual_modnorm_tm(const float* x_in, float* x_out, const vo
                                  RowPerm{n_b, n_t, n_s, h_token_major ? -1 : 0}, tm, stream);
 }
 
+extern "C" int pab_residual_modnorm_peer(const float* x_in, float* x_out, const void* const* pending,
+                                         const int* term_layout, int n_pending, const void* const* peer_src,
+                                         void* peer_copy, const float* gamma, const float* beta,
+                                         const float* mod, void* h_out, void* const* peer_h, int64_t n_b,
+                                         int64_t n_t, int64_t n_s, int64_t n_w, int rank, int D, float eps,
+                                         int mode, int h_layout, void* stream) {
+    if (n_b < 1 || n_t < 1 || n_s < 1 || n_w < 1 || n_w > PAB_MAX_PEERS) return PAB_ERR_SHAPE;
+    if (n_pending < 0 || n_pending > PAB_MAX_PENDING) return PAB_ERR_SHAPE;
+    if (rank < 0 || rank >= n_w) return PAB_ERR_INVALID;
+    TmState tm{0u, n_t, n_s};
+    tm.n_b = n_b;
+    tm.n_w = n_w;
+    tm.me = rank;
+    tm.peer_src = peer_src;
+    tm.copy = peer_copy;
+    bool a2a = h_layout == PAB_LAYOUT_A2A || h_layout == PAB_LAYOUT_PEER;
+    int n_peer = 0;
+    for (int i = 0; i < n_pending; ++i) {
+        const int l = term_layout ? term_layout[i] : PAB_LAYOUT_FRAME;
+        if (l == PAB_LAYOUT_TOKEN) tm.mask |= 1u << i;
+        else if (l == PAB_LAYOUT_A2A) { tm.a2a |= 1u << i; a2a = true; }
+        else if (l == PAB_LAYOUT_PEER) { tm.peer |= 1u << i; a2a = true; ++n_peer; }
+        else if (l != PAB_LAYOUT_FRAME) return PAB_ERR_INVALID;
+    }
+    // one peer-resident term per launch (the temporal output of the preceding site)
+    if (n_peer > 1 || (n_peer == 1 && peer_src == nullptr)) return PAB_ERR_INVALID;
+    if (peer_copy != nullptr && n_peer != 1) return PAB_ERR_INVALID;
+    if (n_peer == 1)
+        for (int w = 0; w < n_w; ++w)
+            if (peer_src[w] == nullptr) return PAB_ERR_INVALID;
+    if (a2a && n_s % n_w != 0) return PAB_ERR_SHAPE;
+    if (h_layout < PAB_LAYOUT_FRAME || h_layout > PAB_LAYOUT_PEER) return PAB_ERR_INVALID;
+    if ((h_layout == PAB_LAYOUT_A2A || h_layout == PAB_LAYOUT_PEER) && mode == 0) return PAB_ERR_INVALID;
+    RowPerm perm{n_b, n_t, n_s,
+                 (h_layout == PAB_LAYOUT_A2A || h_layout == PAB_LAYOUT_PEER) ? n_w
+                                                                             : (h_layout == PAB_LAYOUT_TOKEN ? -1 : 0)};
+    perm.me = rank;
+    if (h_layout == PAB_LAYOUT_PEER) {
+        if (peer_h == nullptr) return PAB_ERR_INVALID;
+        for (int w = 0; w < n_w; ++w) {
+            if (peer_h[w] == nullptr) return PAB_ERR_INVALID;
+            perm.peer[w] = reinterpret_cast<__nv_bfloat16*>(peer_h[w]);
+        }
+    }
+    return residual_modnorm_impl(x_in, x_out, pending, n_pending, gamma, beta, mod, h_out, n_b * n_t * n_s, D, eps,
+                                 mode, perm, tm, stream);
+}
+
 extern "C" int pab_residual_modnorm_ex(const float* x_in, float* x_out, const void* const* pending,
                                        const int* term_layout, int n_pending, const float* gamma,
                                        const float* beta, const float* mod, void* h_out, int64_t n_b,
                                        int64_t n_t, int64_t n_s, int64_t n_w, int D, float eps, int mode,
                                        int h_layout, void* stream) {
-    if (n_b < 1 || n_t < 1 || n_s < 1 || n_w < 1) return PAB_ERR_SHAPE;
-    if (n_pending < 0 || n_pending > PAB_MAX_PENDING) return PAB_ERR_SHAPE;
-    TmState tm{0u, n_t, n_s};
-    tm.n_b = n_b;
-    tm.n_w = n_w;
-    bool a2a = h_layout == PAB_LAYOUT_A2A;
-    for (int i = 0; i < n_pending; ++i) {
-        const int l = term_layout ? term_layout[i] : PAB_LAYOUT_FRAME;
-        if (l == PAB_LAYOUT_TOKEN) tm.mask |= 1u << i;
-        else if (l == PAB_LAYOUT_A2A) { tm.a2a |= 1u << i; a2a = true; }
-        else if (l != PAB_LAYOUT_FRAME) return PAB_ERR_INVALID;
+    if (h_layout == PAB_LAYOUT_PEER) return PAB_ERR_INVALID;
+    for (int i = 0; term_layout && i < n_pending; ++i)
+        if (term_layout[i] == PAB_LAYOUT_PEER) return PAB_ERR_INVALID;
+    if (n_w > PAB_MAX_PEERS) {
+        // plain all-to-all orders work for any W; only the peer forms are bounded
+        bool any = h_layout == PAB_LAYOUT_A2A;
+        for (int i = 0; term_layout && i < n_pending; ++i) any = any || term_layout[i] == PAB_LAYOUT_A2A;
+        if (any) return PAB_ERR_SHAPE;
+        n_w = 1;
     }
-    if (a2a && n_s % n_w != 0) return PAB_ERR_SHAPE;
-    if (h_layout < PAB_LAYOUT_FRAME || h_layout > PAB_LAYOUT_A2A) return PAB_ERR_INVALID;
-    if (h_layout == PAB_LAYOUT_A2A && mode == 0) return PAB_ERR_INVALID;
-    const RowPerm perm{n_b, n_t, n_s, h_layout == PAB_LAYOUT_A2A ? n_w : (h_layout == PAB_LAYOUT_TOKEN ? -1 : 0)};
-    return residual_modnorm_impl(x_in, x_out, pending, n_pending, gamma, beta, mod, h_out, n_b * n_t * n_s, D, eps,
-                                 mode, perm, tm, stream);
+    return pab_residual_modnorm_peer(x_in, x_out, pending, term_layout, n_pending, nullptr, nullptr, gamma, beta,
+                                     mod, h_out, nullptr, n_b, n_t, n_s, n_w, 0, D, eps, mode, h_layout, stream);
 }
 
 static int residual_modnorm_impl(const float* x_in, float* x_out, const void* const* pending,
@@ -423,7 +494,8 @@ static int residual_modnorm_impl(const float* x_in, float* x_out, const void* co
     if (rows < 0 || D <= 0 || n_pending < 0 || n_pending > PAB_MAX_PENDING) return PAB_ERR_SHAPE;
     if (mode < 0 || mode > 2) return PAB_ERR_INVALID;
     if (mode == 1 && mod == nullptr) return PAB_ERR_INVALID;
-    if (mode != 0 && h_out == nullptr) return PAB_ERR_INVALID;
+    const bool peer_h = perm.n_w > 0 && perm.peer[0] != nullptr;
+    if (mode != 0 && h_out == nullptr && !peer_h) return PAB_ERR_INVALID;
     if ((gamma == nullptr) != (beta == nullptr)) return PAB_ERR_INVALID;
     if (rows == 0) return PAB_OK;
     const int write_x = (n_pending > 0 || x_in != x_out) ? 1 : 0;
@@ -437,11 +509,25 @@ static int residual_modnorm_impl(const float* x_in, float* x_out, const void* co
     pl.tm_s = tm.s;
     pl.n_b = tm.n_b;
     pl.n_w = tm.n_w;
+    pl.peer_mask = tm.peer;
+    pl.me = tm.me;
+    if (tm.peer) {
+        for (int w = 0; w < tm.n_w; ++w) pl.peer[w] = reinterpret_cast<const __nv_bfloat16*>(tm.peer_src[w]);
+        if (tm.copy) {
+            pl.copy = reinterpret_cast<__nv_bfloat16*>(tm.copy);
+            for (int i = 0; i < n_pending; ++i)
+                if (tm.peer & (1u << i)) pl.copy_term = i;
+        }
+    }
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     auto* h = reinterpret_cast<__nv_bfloat16*>(h_out);
     bool aligned = (D % 4 == 0) && ((uintptr_t)x_in % 16 == 0) && ((uintptr_t)x_out % 16 == 0) &&
                    (h == nullptr || (uintptr_t)h % 8 == 0);
-    for (int i = 0; i < n_pending; ++i) aligned = aligned && ((uintptr_t)pending[i] % 8 == 0);
+    for (int i = 0; i < n_pending; ++i)
+        aligned = aligned && ((tm.peer >> i) & 1u ? true : (uintptr_t)pending[i] % 8 == 0);
+    for (int w = 0; w < PAB_MAX_PEERS; ++w)
+        aligned = aligned && (uintptr_t)pl.peer[w] % 8 == 0 && (uintptr_t)perm.peer[w] % 8 == 0;
+    aligned = aligned && (uintptr_t)pl.copy % 8 == 0;
     if (aligned)
         return launch_modnorm_vec<4>(x_in, x_out, pl, gamma, beta, mod, h, rows, D, eps, mode, write_x, perm, st);
     return launch_modnorm_vec<1>(x_in, x_out, pl, gamma, beta, mod, h, rows, D, eps, mode, write_x, perm, st);

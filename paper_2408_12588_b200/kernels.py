@@ -31,7 +31,7 @@ def _need(t: torch.Tensor, dtype, name: str):
         raise ValidationError(f"{name} must be {dtype}, got {t.dtype}")
 
 
-LAYOUT_FRAME, LAYOUT_TOKEN, LAYOUT_A2A = 0, 1, 2
+LAYOUT_FRAME, LAYOUT_TOKEN, LAYOUT_A2A, LAYOUT_PEER = 0, 1, 2, 3
 
 
 def is_token_major(t) -> bool:
@@ -42,18 +42,25 @@ def is_token_major(t) -> bool:
 def term_layout(t) -> int:
     """Row layout of a pending residual term: frame-major, token-major (serial temporal
     site) or all-to-all order (sequence-parallel temporal site, ``pab_a2a_world`` ranks)."""
+    if getattr(t, "pab_peer", None) is not None:
+        return LAYOUT_PEER
     if getattr(t, "pab_a2a_world", 0):
         return LAYOUT_A2A
     return LAYOUT_TOKEN if is_token_major(t) else LAYOUT_FRAME
 
 
 def residual_modnorm(x_in, x_out, pending, h_out=None, mod=None, gamma=None, beta=None, mode=1, eps=1e-5,
-                     shape=None, h_token_major=False, h_layout=None, n_w=1):
+                     shape=None, h_token_major=False, h_layout=None, n_w=1, h_peer=None):
     """x_out = x_in + sum(pending) (fp32); h_out = modnorm(x_out) (mode 1) or bf16(x_out) (mode 2).
 
     ``shape`` = (B, T, S) of the residual stream (block); needed when a pending term is not
     frame-major (``term_layout``) or when h is written token-major (``h_token_major``) or in
     all-to-all send order over ``n_w`` ranks (``h_layout=LAYOUT_A2A``).
+
+    Peer transport (broadcast SP over NVLink, ``peer.PeerExchange``): ``h_peer`` = (exchange,
+    buffer name) stores h straight into every rank's token-layout buffer (``LAYOUT_PEER``);
+    a pending term carrying ``pab_peer`` = (exchange, buffer name) is read out of the ranks'
+    buffers, and copied frame-major into ``pab_peer_copy`` when that is set (cache slot).
     """
     lib = _lib.load()
     _need(x_in, torch.float32, "x_in")
@@ -71,8 +78,14 @@ def residual_modnorm(x_in, x_out, pending, h_out=None, mod=None, gamma=None, bet
         if h_out.numel() != x_in.numel():
             raise ShapeError("h_out does not match the residual stream")
     if h_layout is None:
-        h_layout = LAYOUT_TOKEN if h_token_major else LAYOUT_FRAME
+        h_layout = LAYOUT_PEER if h_peer is not None else (LAYOUT_TOKEN if h_token_major else LAYOUT_FRAME)
     layouts = [term_layout(p) for p in pending]
+    peer_terms = [p for p, lay in zip(pending, layouts) if lay == LAYOUT_PEER]
+    if len(peer_terms) > 1:
+        raise ValidationError("at most one peer-resident pending term per prologue")
+    px = h_peer[0] if h_peer is not None else (peer_terms[0].pab_peer[0] if peer_terms else None)
+    if px is not None:
+        n_w = px.world
     for p, lay in zip(pending, layouts):
         if lay == LAYOUT_A2A:
             n_w = int(p.pab_a2a_world)
@@ -80,11 +93,24 @@ def residual_modnorm(x_in, x_out, pending, h_out=None, mod=None, gamma=None, bet
     if general and (shape is None or shape[0] * shape[1] * shape[2] != rows):
         raise ShapeError("permuted residual terms / outputs need the (B, T, S) shape of the stream")
     pend = list(zip(pending, layouts))
-    src = x_in
+    src_x = [x_in]
 
     def call(terms, h, m, md, hl):
         arr = _lib.ptr_array([p.data_ptr() for p, _ in terms])
         ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        peer_in = [p for p, l in terms if l == LAYOUT_PEER]
+        if px is not None and (peer_in or hl == LAYOUT_PEER):
+            lay = (ctypes.c_int * max(1, len(terms)))(*[l for _, l in terms])
+            src = px.ptrs(peer_in[0].pab_peer[1]) if peer_in else None
+            copy = getattr(peer_in[0], "pab_peer_copy", None) if peer_in else None
+            dst = px.ptrs(h_peer[1]) if hl == LAYOUT_PEER else None
+            st = lib.pab_residual_modnorm_peer(src_x[0].data_ptr(), x_out.data_ptr(), arr, lay, len(terms), src,
+                                               ptr(copy), ptr(gamma), ptr(beta), ptr(md), ptr(h), dst, shape[0],
+                                               shape[1], shape[2], int(n_w), int(px.rank), D, float(eps), int(m),
+                                               int(hl), _stream())
+            _lib.check(st, "pab_residual_modnorm_peer")
+            return
+        src = src_x[0]
         if general:
             lay = (ctypes.c_int * max(1, len(terms)))(*[l for _, l in terms])
             st = lib.pab_residual_modnorm_ex(src.data_ptr(), x_out.data_ptr(), arr, lay, len(terms), ptr(gamma),
@@ -100,7 +126,7 @@ def residual_modnorm(x_in, x_out, pending, h_out=None, mod=None, gamma=None, bet
     while len(pend) > MAX_PENDING:
         chunk, pend = pend[:MAX_PENDING], pend[MAX_PENDING:]
         call(chunk, None, 0, None, LAYOUT_FRAME)
-        src = x_out
+        src_x[0] = x_out
     call(pend, h_out, mode, mod, h_layout)
 
 

@@ -47,6 +47,9 @@ from .policies import CacheStore, DecisionTable, PabPolicy, PolicyConfig, build_
 
 METHOD_COSTS = {"megatron_sp": 16, "ds_ulysses": 4, "dsp": 2, "broadcast_sp": 2}
 EXECUTABLE_METHODS = ("dsp", "broadcast_sp")
+# how the temporal site's two reshards move data: NCCL all-to-alls, or stores/loads over
+# NVLink peer memory fused into the prologues (peer.py)
+TRANSPORTS = ("nccl", "peer")
 TM = ComponentKind.TEMPORAL
 
 
@@ -196,6 +199,7 @@ class _LocalGroupState:
         self.size = size
         self.barrier = threading.Barrier(size, timeout=600)
         self.slots = [None] * size
+        self.events = [None] * size  # CUDA event per member: its posted data / its reads are done
 
 
 class LocalGroup:
@@ -206,8 +210,10 @@ class LocalGroup:
     ``run_parallel`` runs them as W threads on one GPU and exchanges shards
     through this group: every member posts its send buffer, waits at a barrier,
     copies its chunks from the peers' buffers and waits again before any buffer
-    can be rewritten.  All threads enqueue on the device's default stream, so
-    the copies are ordered after the producing kernels by issue order."""
+    can be rewritten.  Device ordering follows the host barriers through CUDA
+    events: a reader's stream waits for the poster's event before copying, and a
+    poster's stream waits for every reader's event before it may rewrite (so the
+    members may issue on different streams, as the peer transport does)."""
 
     def __init__(self, state: _LocalGroupState, rank: int):
         self.state, self.rank = state, rank
@@ -215,22 +221,45 @@ class LocalGroup:
     def size(self) -> int:
         return self.state.size
 
-    def _post(self, t):
+    def _record(self):
+        import torch
+
+        if not torch.cuda.is_available() or not torch.cuda.is_initialized():
+            return
+        ev = torch.cuda.Event()
+        ev.record()
+        self.state.events[self.rank] = ev
+
+    def _wait_all(self):
+        import torch
+
+        if not torch.cuda.is_available() or not torch.cuda.is_initialized():
+            return
+        cur = torch.cuda.current_stream()
+        for w, ev in enumerate(self.state.events):
+            if w != self.rank and ev is not None:
+                cur.wait_event(ev)
+
+    def _sync(self):
         st = self.state
-        st.slots[self.rank] = t
         try:
             st.barrier.wait()
         except Exception:
             st.barrier.abort()
             raise
 
+    def _post(self, t):
+        self.state.slots[self.rank] = t
+        self._record()
+        self._sync()
+        self._wait_all()  # the posted tensors are complete on the device
+        self._sync()      # nobody re-records its event before everyone has waited on it
+
     def _done(self):
-        st = self.state
-        try:
-            st.barrier.wait()
-        except Exception:
-            st.barrier.abort()
-            raise
+        self._record()
+        self._sync()
+        self._wait_all()  # every member's reads of my posted tensor are done
+        self._sync()
 
     def all_to_all_single(self, recv, send):
         """send (W, ...) by destination -> recv (W, ...) by source."""
@@ -240,6 +269,13 @@ class LocalGroup:
         for src in range(W):
             rv[src].copy_(self.state.slots[src].reshape(W, -1)[me])
         self._done()
+
+    def exchange_objects(self, obj):
+        """Every member's ``obj`` in rank order (the peer transport's pointer exchange)."""
+        self._post(obj)
+        out = list(self.state.slots)
+        self._done()
+        return out
 
     def all_gather(self, t):
         self._post(t)
@@ -333,12 +369,16 @@ def unpack_frames(recv, out):
 class _SPTemporal:
     """Token-layout workspaces + the temporal-site hook for run_forward."""
 
-    def __init__(self, ctx, world: int, group, ledger: CommReport, bytes_per_element: int, groups: int = 1):
+    def __init__(self, ctx, world: int, group, ledger: CommReport, bytes_per_element: int, groups: int = 1,
+                 transport: str = "nccl", rank: int = 0):
         import torch
 
         from . import kernels
 
+        if transport not in TRANSPORTS:
+            raise ValidationError(f"transport must be one of {TRANSPORTS}, got {transport!r}")
         self.ctx, self.W, self.group, self.ledger = ctx, world, group, ledger
+        self.transport, self.rank = transport, rank
         B, Tl, S, D = ctx.B, ctx.T, ctx.S, ctx.D
         T, Sw = Tl * world, S // world
         self.T, self.Sw = T, Sw
@@ -346,12 +386,21 @@ class _SPTemporal:
         bf = dict(device=dev, dtype=torch.bfloat16)
         rows_tok = T * B * Sw  # == ctx.rows
         self.h_send = ctx.h.view(world, Tl, B, Sw, D)
-        self.h_tok = torch.empty((T, B, Sw, D), **bf)
         self.qkv_tok = torch.empty((rows_tok, 3 * D), **bf)
         self.attn_tok = torch.empty((rows_tok, D), **bf)
-        self.o_tok = torch.empty((T, B, Sw, D), **bf)
-        self.o_recv = torch.empty((world, Tl, B, Sw, D), **bf)
-        self.o_recv.pab_a2a_world = world
+        if transport == "peer":
+            # token-layout buffers every rank maps: peers store h into h_tok, read o out of o_tok
+            from .peer import PeerExchange
+
+            self.px = PeerExchange(group, rank, world, {"h_tok": ((T, B, Sw, D), torch.bfloat16),
+                                                        "o_tok": ((T, B, Sw, D), torch.bfloat16)}, dev)
+            self.h_tok, self.o_tok = self.px.local["h_tok"], self.px.local["o_tok"]
+        else:
+            self.px = None
+            self.h_tok = torch.empty((T, B, Sw, D), **bf)
+            self.o_tok = torch.empty((T, B, Sw, D), **bf)
+            self.o_recv = torch.empty((world, Tl, B, Sw, D), **bf)
+            self.o_recv.pab_a2a_world = world
         q, k, v = self.qkv_tok[:, :D], self.qkv_tok[:, D:2 * D], self.qkv_tok[:, 2 * D:]
         ld = 3 * D
         # token layout rows (t, b, s): problem (a = b, b_idx = s), rows i = t (stride B*Sw rows)
@@ -372,6 +421,9 @@ class _SPTemporal:
         ctx, d = self.ctx, st.decisions
         source = d.source(li, TM)
         site = (li, TM, "t")
+        if source == st.step and self.px is not None:
+            self._compute_peer(st, li, lp, d.should_store(li, TM))
+            return
         if source == st.step:
             store = d.should_store(li, TM)
             p = lp.temporal
@@ -408,6 +460,41 @@ class _SPTemporal:
         st.pending.append(o)
         st.record(li, TM, "t", decision, source, o)
 
+    def _compute_peer(self, st, li, lp, store):
+        """Computed temporal site over NVLink peer memory: the prologue's stores are the
+        frames->tokens exchange, the next prologue's loads the tokens->frames one."""
+        import torch
+
+        from . import kernels
+        from .model import MOD_TEMPORAL
+
+        ctx, p, px = self.ctx, lp.temporal, self.px
+        if st.wants_output():
+            raise ValidationError("output digests/snapshots are not available with the peer transport")
+        kernels.residual_modnorm(st.src.view(-1, ctx.D), st.r.view(-1, ctx.D), st.pending, mod=st.mods[li, MOD_TEMPORAL],
+                                 mode=1, shape=(ctx.B, ctx.T, ctx.S), h_peer=(px, "h_tok"))
+        ctx.launches.prologue_calls += 1
+        st.src, st.pending = st.r, []
+        px.barrier()  # every rank's h rows have landed in every h_tok
+        self._log(st.step, li)
+        kernels.gemm(self.h_tok.view(-1, ctx.D), p.w_qkv_t, self.qkv_tok)
+        kernels.attention(self.args, ctx.attn_impl)
+        kernels.gemm(self.attn_tok, p.wo_t, self.o_tok.view(-1, ctx.D))
+        px.barrier()  # every rank's o_tok is complete (and every h_tok read)
+        self._log(st.step, li)
+        o = self.o_tok.view(self.o_tok.shape)  # a fresh view object carries the peer marker
+        o.pab_peer = (px, "o_tok")
+        if store:
+            slot = torch.empty((ctx.B, ctx.T, ctx.S, ctx.D), device=o.device, dtype=torch.bfloat16)
+            o.pab_peer_copy = slot  # filled frame-major by the prologue that consumes o
+            st.cache.store((li, TM, "t"), slot, st.step, "outputs")
+        ctx.launches.attention_calls += 1
+        ctx.launches.gemm_calls += 2
+        ctx.launches.other_calls += 2
+        ctx.launches.sites_computed += 1
+        st.pending.append(o)
+        st.record(li, TM, "t", "compute", st.step, o)
+
     def _log(self, step, layer):
         for _ in range(self.groups):
             self.ledger.entries.append(CommEntry(step, layer, self.ledger.method, self.el, self.el * self.bpe,
@@ -421,7 +508,8 @@ class ShardedDenoiser(GraphReplay):
     def __init__(self, params: ModelParams, schedule, table: DecisionTable, text_ids, *, guidance: bool,
                  guidance_scale: float, rank: int, world: int, group=None, method: str = "broadcast_sp",
                  noise_params: NoiseParams = DEFAULT_NOISE, bytes_per_element: int = 4, trace=None,
-                 half: Optional[int] = None, cfg_group=None, total_workers: Optional[int] = None):
+                 half: Optional[int] = None, cfg_group=None, total_workers: Optional[int] = None,
+                 transport: str = "nccl"):
         """rank/world/group: this rank's position in its sequence-parallel group.
         split_batch: half = 0 (conditional) / 1 (unconditional) CFG half run by this
         group, cfg_group = the 2-rank group {cond rank, uncond rank} of these frames."""
@@ -447,7 +535,9 @@ class ShardedDenoiser(GraphReplay):
                        for i, t in enumerate(ts)]
         self.ctx = StepContext.build(params, self.batch, self.ids, ts, frames=self.plan.frames_per_worker)
         self.ledger = CommReport(method, total_workers or world, bytes_per_element, METHOD_COSTS[method])
-        self.hook = (_SPTemporal(self.ctx, world, group, self.ledger, bytes_per_element, 2 if split else 1)
+        self.transport = transport
+        self.hook = (_SPTemporal(self.ctx, world, group, self.ledger, bytes_per_element, 2 if split else 1,
+                                 transport=transport, rank=rank)
                      if world > 1 else None)
         self.cache = CacheStore()
         self.trace = trace
@@ -525,7 +615,7 @@ class ShardedDenoiser(GraphReplay):
 
 def split_batch_denoiser(params: ModelParams, schedule, table: DecisionTable, text_ids, *, guidance_scale: float,
                          method: str = "broadcast_sp", noise_params: NoiseParams = DEFAULT_NOISE,
-                         bytes_per_element: int = 4, trace=None) -> "ShardedDenoiser":
+                         bytes_per_element: int = 4, trace=None, transport: str = "nccl") -> "ShardedDenoiser":
     """Collective (every rank calls it): CFG halves on two rank groups of W/2
     (reference parallel.py:410-434).  Ranks [0, W/2) run the conditional half,
     [W/2, W) the unconditional one; rank w and W/2 + w hold the same frames."""
@@ -542,7 +632,7 @@ def split_batch_denoiser(params: ModelParams, schedule, table: DecisionTable, te
     return ShardedDenoiser(params, schedule, table, text_ids, guidance=True, guidance_scale=guidance_scale,
                            rank=w, world=gw, group=sp[half], method=method, noise_params=noise_params,
                            bytes_per_element=bytes_per_element, trace=trace, half=half, cfg_group=pairs[w],
-                           total_workers=world)
+                           total_workers=world, transport=transport)
 
 
 @dataclass
@@ -601,6 +691,7 @@ def run_parallel(
     noise_params: NoiseParams = DEFAULT_NOISE,
     table: Optional[DecisionTable] = None,
     bytes_per_element: int = 4,
+    transport: str = "nccl",
 ) -> ParallelRunResult:
     """Sequence-parallel sampler (reference parallel.run_parallel, parallel.py:372-464).
 
@@ -609,7 +700,9 @@ def run_parallel(
     gathered full latent.  Without a process group, ``workers`` logical
     workers run in this process on the current GPU, as the reference runs
     them (one thread per worker, shards exchanged through ``LocalGroup``);
-    ``workers == 1`` is the single-GPU engine.
+    ``workers == 1`` is the single-GPU engine.  ``transport`` (B200 extension):
+    "nccl" runs the temporal site's reshards as all-to-alls, "peer" as stores and
+    loads over NVLink peer memory fused into the prologues (peer.py).
     """
     import torch
     import torch.distributed as dist
@@ -619,6 +712,8 @@ def run_parallel(
         raise ValidationError(f"method {method!r} is not executable; use comm_volume_model for it")
     if method == "broadcast_sp" and not isinstance(policy, PabPolicy):
         raise ValidationError("broadcast_sp requires a PAB policy")
+    if transport not in TRANSPORTS:
+        raise ValidationError(f"transport must be one of {TRANSPORTS}, got {transport!r}")
     if table is None:
         table = build_schedule(policy, schedule, cfg.layers, range_semantics=range_semantics)
     if text_ids is None:
@@ -626,7 +721,7 @@ def run_parallel(
     multi = dist.is_available() and dist.is_initialized()
     if not multi and workers > 1:
         return _run_logical(params, schedule, table, text_ids, workers, method, seed, guidance, guidance_scale,
-                            split_batch, noise_params, bytes_per_element)
+                            split_batch, noise_params, bytes_per_element, transport)
     world = dist.get_world_size() if multi else 1
     rank = dist.get_rank() if multi else 0
     if workers != world:
@@ -635,17 +730,20 @@ def run_parallel(
     use_split = bool(split_batch and guidance and workers >= 2 and workers % 2 == 0)
     if use_split:
         den = split_batch_denoiser(params, schedule, table, text_ids, guidance_scale=guidance_scale,
-                                   method=method, noise_params=noise_params, bytes_per_element=bytes_per_element)
+                                   method=method, noise_params=noise_params, bytes_per_element=bytes_per_element,
+                                   transport=transport)
     else:
         den = ShardedDenoiser(params, schedule, table, text_ids, guidance=guidance, guidance_scale=guidance_scale,
                               rank=rank, world=world, method=method, noise_params=noise_params,
-                              bytes_per_element=bytes_per_element)
+                              bytes_per_element=bytes_per_element, transport=transport)
     batch = 2 if guidance else 1
     x_full = torch.from_numpy(initial_latent(params, seed, batch)).to(params.w_time.device)
     if use_split:
         x_full = x_full[den.half:den.half + 1]
     z = den.shard_input(x_full)
     den.run(z)
+    if den.hook is not None and den.hook.px is not None:
+        den.hook.px.check()
     if world > 1:
         parts = _all_gather(z)
         if use_split:
@@ -664,8 +762,10 @@ def run_parallel(
 
 
 def _run_logical(params, schedule, table, text_ids, workers, method, seed, guidance, guidance_scale, split_batch,
-                 noise_params, bytes_per_element) -> ParallelRunResult:
-    """W logical workers on this process's GPU (threads exchanging through LocalGroup)."""
+                 noise_params, bytes_per_element, transport="nccl") -> ParallelRunResult:
+    """W logical workers on this process's GPU (threads exchanging through LocalGroup).
+    With the peer transport each worker issues on its own CUDA stream (the device
+    barriers of one worker must not block the others' kernels)."""
     import threading
 
     import torch
@@ -690,10 +790,16 @@ def _run_logical(params, schedule, table, text_ids, workers, method, seed, guida
                       bytes_per_element=bytes_per_element)
             if use_split:
                 kw.update(half=half, cfg_group=LocalGroup(pairs[r], half), total_workers=workers)
-            den = ShardedDenoiser(params, schedule, table, text_ids, **kw)
-            dens[w] = den
-            z = den.shard_input(x_full[half:half + 1] if use_split else x_full)
-            den.run(z)
+            stream = torch.cuda.Stream(dev) if transport == "peer" else torch.cuda.current_stream(dev)
+            stream.wait_stream(torch.cuda.default_stream(dev))
+            with torch.cuda.stream(stream):
+                den = ShardedDenoiser(params, schedule, table, text_ids, transport=transport, **kw)
+                dens[w] = den
+                z = den.shard_input(x_full[half:half + 1] if use_split else x_full)
+                den.run(z)
+                stream.synchronize()
+                if den.hook is not None and den.hook.px is not None:
+                    den.hook.px.check()
             outs[w] = z
         except BaseException as e:  # noqa: BLE001 - re-raised on the calling thread
             errs.append(e)

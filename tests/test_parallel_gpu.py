@@ -26,7 +26,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, guidance, split, q):
+def _worker(rank, world, port, guidance, split, q, transport="nccl"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -43,7 +43,7 @@ def _worker(rank, world, port, guidance, split, q):
         pol = PabPolicy(2, 3, 2, window=(990.0, 10.0))
         table = build_schedule(pol, sched, cfg.layers)
         par = run_parallel(params, sched, pol, world, "broadcast_sp", seed=7, guidance=guidance, table=table,
-                           split_batch=split)
+                           split_batch=split, transport=transport)
         gathered = par.gathered_cache()
         out = {"rank": rank}
         if rank == 0:
@@ -139,6 +139,90 @@ def test_logical_workers_without_process_group(world, guidance, split):
                               split_batch=split)
     assert par.comm_report.grouped_elements() == model.grouped_elements()
     assert len(par.worker_caches) == world and len(par.gathered_cache()) > 0
+
+
+@pytest.mark.parametrize("world,guidance,split", [(2, False, False), (4, True, False), (8, True, False),
+                                                  (4, True, True)])
+def test_peer_transport_logical_workers(world, guidance, split):
+    """The NVLink peer transport (peer.py: h stored straight into the ranks' token
+    buffers by the temporal prologue, o read straight out of them by the next
+    prologue, device barriers in between) against the all-to-all transport: same
+    kernels, same summation order, so the latents and every cache slot are
+    bit-identical; the ledger (reference element counts) is unchanged."""
+    from paper_2408_12588_b200.diffusion import make_schedule
+    from paper_2408_12588_b200.model import ComponentKind, ModelConfig, init_model
+    from paper_2408_12588_b200.parallel import run_parallel
+    from paper_2408_12588_b200.policies import PabPolicy, build_schedule
+
+    cfg = ModelConfig(layers=2, hidden=144, heads=2, frames=8, spatial_tokens=64, text_tokens=12,
+                      cross_in_temporal=True)
+    params = init_model(cfg, seed=3)
+    sched = make_schedule(8)
+    pol = PabPolicy(2, 3, 2, window=(990.0, 10.0))
+    table = build_schedule(pol, sched, cfg.layers)
+    kw = dict(seed=7, guidance=guidance, table=table, split_batch=split)
+    a2a = run_parallel(params, sched, pol, world, "broadcast_sp", transport="nccl", **kw)
+    peer = run_parallel(params, sched, pol, world, "broadcast_sp", transport="peer", **kw)
+    assert np.array_equal(a2a.latent, peer.latent)
+    ca, cp = a2a.gathered_cache(), peer.gathered_cache()
+    assert ca.keys() == cp.keys() and len(cp) > 0
+    for site in ca:
+        assert np.array_equal(ca[site], cp[site]), site
+    groups = 2 if split else 1
+    comp = table.compute_steps(ComponentKind.TEMPORAL)
+    assert peer.comm_report.event_count() == 2 * cfg.layers * len(comp) * groups
+    assert peer.comm_report.grouped_elements() == a2a.comm_report.grouped_elements()
+
+
+def test_peer_transport_processes_ipc():
+    """Two processes share cuda:0 and map each other's token buffers through CUDA IPC
+    (the production multi-process path; on a B200 box the same handles map peer GPUs
+    over NVLink).  Checked against the serial engine, with the ledger and cache."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    world = 2
+    procs = [ctx.Process(target=_worker, args=(r, world, port, True, False, q, "peer")) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    errs = [r for r in res if "error" in r]
+    assert not errs, errs
+    r0 = [r for r in res if r["rank"] == 0][0]
+    assert r0["rel"] < 2e-3, r0
+    assert r0["events"] == r0["events_want"] and r0["steps_ok"] and r0["ledger_ok"], r0
+    assert r0["n_cache"] > 0 and r0["cache_rel"] < 2e-3, r0
+
+
+def test_peer_barrier_timeout_reports_instead_of_hanging():
+    """A rank that never arrives: the device barrier gives up at its deadline and
+    records PAB_PEER_TIMEOUT (no GPU hang), which PeerExchange.check raises."""
+    from paper_2408_12588_b200.errors import DeviceError
+    from paper_2408_12588_b200.parallel import LocalGroup, _LocalGroupState
+    from paper_2408_12588_b200.peer import PEER_TIMEOUT, PeerExchange
+
+    import threading
+
+    st = _LocalGroupState(2)
+    out = [None, None]
+
+    def mk(w):
+        torch.cuda.set_device(0)
+        out[w] = PeerExchange(LocalGroup(st, w), w, 2, {"b": ((4,), torch.float32)}, "cuda:0", timeout_s=0.2)
+
+    ts = [threading.Thread(target=mk, args=(w,)) for w in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    px = out[0]
+    px.barrier()  # rank 1 never calls it
+    torch.cuda.synchronize()
+    assert int(px.error.item()) == PEER_TIMEOUT
+    with pytest.raises(DeviceError):
+        px.check()
 
 
 def _nccl_worker(rank, world, port, q):
