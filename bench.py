@@ -274,6 +274,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-none", action="store_true", help="skip the no-PAB comparison run")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of replaying a CUDA graph")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
+                    help="N>1: temporal-site reshards as NCCL all-to-alls, or fused into the prologues as "
+                         "stores/loads over NVLink peer memory (peer.py)")
     ap.add_argument("--split-batch", action="store_true",
                     help="N>1: CFG halves on two rank groups of N/2 (reference run_parallel split_batch)")
     args = ap.parse_args()
@@ -318,12 +321,12 @@ def main():
         if split:
             from paper_2408_12588_b200.parallel import split_batch_denoiser
 
-            return split_batch_denoiser(params, sched, tab, ids, guidance_scale=4.0)
+            return split_batch_denoiser(params, sched, tab, ids, guidance_scale=4.0, transport=args.transport)
         if world > 1:
             from paper_2408_12588_b200.parallel import ShardedDenoiser
 
             return ShardedDenoiser(params, sched, tab, ids, guidance=guidance, guidance_scale=4.0, rank=rank,
-                                   world=world)
+                                   world=world, transport=args.transport)
         return Denoiser(params, sched, tab, ids, guidance=guidance, guidance_scale=4.0)
 
     den = make_denoiser(table)
@@ -343,7 +346,8 @@ def main():
     # one CUDA graph per video; under torchrun with NCCL the all-to-alls are captured too
     # (a gloo group -- several ranks sharing one GPU in tests -- cannot be captured)
     backend = os.environ.get("PAB_DIST_BACKEND", "nccl")
-    use_graph = not args.no_graph and (world == 1 or backend == "nccl")
+    # (the peer transport has no collective inside the loop, so it captures under gloo too)
+    use_graph = not args.no_graph and (world == 1 or backend == "nccl" or (args.transport == "peer" and not split))
 
     def denoise(d, zz):
         return d.run_graph(zz) if use_graph else d.run(zz)
@@ -486,7 +490,16 @@ def main():
     # all-to-all traffic of one video: calls and bytes from the run's
     # ledger, the per-call time from the same exchange timed alone (CUDA events, max over ranks)
     a2a = None
-    if world > 1 and getattr(den, "hook", None) is not None:
+    if world > 1 and getattr(den, "hook", None) is not None and den.hook.px is not None:
+        hook = den.hook
+        a2a = {"transport": "peer", "calls_per_video": 0,
+               "barriers_per_video": den.ledger.event_count() // (2 if split else 1),
+               "exchange_bytes_per_video_per_rank": hook.wire * den.ledger.event_count() // (2 if split else 1),
+               "note": "no all-to-all: the temporal prologue stores h into the ranks' token buffers and the next "
+                       "prologue reads o out of them over NVLink peer memory; one device barrier per exchange",
+               "skipped_on_temporal_broadcast_steps": True,
+               "ledger_elements_per_video": den.ledger.total_elements()}
+    elif world > 1 and getattr(den, "hook", None) is not None:
         hook = den.hook
         calls = den.ledger.event_count() // (2 if split else 1)
         send_b = hook.h_send.numel() * hook.h_send.element_size()
@@ -504,7 +517,7 @@ def main():
         t = torch.tensor([a_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         a_ms = float(t.item())
-        a2a = {"calls_per_video": calls, "bytes_per_call_per_rank": send_b,
+        a2a = {"transport": "nccl", "calls_per_video": calls, "bytes_per_call_per_rank": send_b,
                "wire_bytes_per_call_per_rank": hook.wire, "ms_per_call": a_ms,
                "est_ms_per_video": a_ms * calls, "skipped_on_temporal_broadcast_steps": True,
                "ledger_elements_per_video": den.ledger.total_elements()}
@@ -573,6 +586,7 @@ def main():
                        "denoise_steps": c["steps"], "batch": c["batch"], "preset": c["preset"],
                        "parallelism": (f"cfg2x_broadcast_sp{world // 2}" if split else
                                        f"broadcast_sp{world}" if world > 1 else "single"),
+                       "transport": args.transport if world > 1 else None,
                        "l2": "inputs larger than L2 (fp32 latent 230 MB > 126 MB L2)",
                        "launch": ("one CUDA graph per video (static decision table)" if use_graph
                                   else graph_note or "eager"),
