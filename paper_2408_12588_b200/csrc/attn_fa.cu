@@ -53,7 +53,20 @@ using namespace pab::tc;
 #endif
 constexpr int kSplit = PAB_FA_SPLIT;
 constexpr int kSoftmaxWarps = 8 * kSplit;
-constexpr int kThreads = 32 * (kSoftmaxWarps + 3);
+
+#ifndef PAB_FA_EPI_WARPS
+#define PAB_FA_EPI_WARPS 1  // 1: O epilogue on 4 dedicated warps (registers rebalanced with setmaxnreg)
+#endif
+// Dedicated epilogue warps (round 2): warps 12..15 (TMEM lane quarters 0..3) drain each
+// finished item's O while the softmax warps already run the next item (the epilogue
+// was 18% of cross and 7% of spatial time on the softmax warps' critical path,
+// measured with PAB_FA_DIAG_NOEPI).  512 threads: the softmax warpgroups raise their
+// register budget to kRegSoftmax, the MMA / TMA / fixer / epilogue warpgroups lower theirs.
+constexpr bool kEpiWarps = PAB_FA_EPI_WARPS != 0 && kSplit == 1;
+constexpr int kEpiWarp0 = 12;
+constexpr int kThreads = kEpiWarps ? 512 : 32 * (kSoftmaxWarps + 3);
+constexpr int kRegSoftmax = 176, kRegAux = 80;
+static_assert(!kEpiWarps || 256 * kRegSoftmax + 256 * kRegAux <= 65536, "register file");
 constexpr int kRows = 128;   // query rows per tile == TMEM lanes
 constexpr int kKv = 112;     // keys per KV tile
 constexpr int kHalf = kKv / kSplit;  // score columns per softmax thread
@@ -80,6 +93,7 @@ constexpr uint32_t kSCol = 0, kPCol = 384;
 #define PAB_FA_PV_SPLIT 1  // 1: P.V issued per query tile (own p_full / o_done), 0: one group for both
 #endif
 constexpr bool kPvSplit = PAB_FA_PV_SPLIT != 0;
+static_assert(!kEpiWarps || kPvSplit, "the dedicated epilogue needs per-tile o_done / o_final");
 
 #ifndef PAB_FA_POLY_DIV
 #define PAB_FA_POLY_DIV 3   // one column pair in PAB_FA_POLY_DIV on the FMA pipe (0: MUFU only)
@@ -141,6 +155,7 @@ struct Bars {
     uint64_t q_ready[2], k_ready[3];  // Q / K tiles after the fixer warp's pad-column patch
     uint64_t s_full, s_free;         // shared by the two query tiles (S is one interleaved MMA group)
     uint64_t p_full[2], o_done[2];   // per tile (PAB_FA_PV_SPLIT) or index 0 for both
+    uint64_t o_final[2], o_free[2];  // dedicated epilogue: item's last P.V done / O read out of TMEM
 };
 
 // single-thread tcgen05.mma issue (lane 0 of the MMA warp): descriptors are passed as
@@ -401,6 +416,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = 0; t < 2; ++t) {
             mbar_init(&bars->p_full[t], kPvSplit ? kSoftmaxWarps / 2 : kSoftmaxWarps);
             mbar_init(&bars->o_done[t], 1);
+            mbar_init(&bars->o_final[t], 1);
+            mbar_init(&bars->o_free[t], 4);  // one arrival per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -415,6 +432,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     // the CTA allocates all 512 columns, so the TMEM base address is lane 0 / column 0
     constexpr uint32_t tmem = 0;
+    if (kEpiWarps) {
+        if (warp < kSoftmaxWarps) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
+        else asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegAux));
+    }
 
     if (warp < kSoftmaxWarps) {
         // ========================================= softmax + epilogue of query tile t
@@ -439,6 +460,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t xbar = 1 + 4 * t + wl;  // named barrier of the two warps sharing these rows
         // O of the previous item of this tile -> normalised bf16 rows (its last P.V done)
         auto epilogue = [&](const Item& it) {
+#ifdef PAB_FA_DIAG_NOEPI  // timing diagnostic only: no epilogue at all (O never leaves TMEM)
+            return;
+#endif
             float o[16];
             PAB_TMEM_LD16(o_tmem + 16 * (p.dh / 16), o);  // row sum sits in column dh
             tmem_wait_ld();
@@ -638,7 +662,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&bars->o_done[tb], (it_n - 1) & 1);
                     tc_fence_after();
                 }
-                if (j == 0 && have_prev) epilogue(prev);  // O of the previous item is final
+                if (!kEpiWarps && j == 0 && have_prev) epilogue(prev);  // O of the previous item is final
                 if (kSplit == 1) {
                     PAB_TMEM_ST16U(p_tmem, pk);
                     PAB_TMEM_ST16U(p_tmem + 16, (pk + 16));
@@ -660,12 +684,84 @@ __global__ void __launch_bounds__(kThreads, 1)
                 have_prev = true;
             }
         }
-        if (have_prev) {
+        if (!kEpiWarps && have_prev) {
             mbar_wait(&bars->o_done[tb], (it_n - 1) & 1);
             tc_fence_after();
             epilogue(prev);
         }
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // tile stores complete before exit
+    } else if (kEpiWarps && warp >= kEpiWarp0) {
+        // ================================= dedicated epilogue (warp = kEpiWarp0 + lane quarter)
+        // per item and tile: wait for the item's last P.V (o_final), read the row sum and O out
+        // of TMEM in 16-column chunks into the dense staging rows, hand O back to the MMA warp
+        // (o_free: the next item's first P.V overwrites it), then one thread issues the tile's
+        // TMA tensor store.  Off the softmax warps' critical path.
+        const int wl = warp & 3;
+        const int row = wl * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(wl * 32) << 16;
+        const bool issuer = (wl == 0 && lane == 0);
+        int last_t = -1;  // staging tile of the issuer's most recent bulk store
+        for (int c = 0; c < my_items; ++c) {
+            const Item it = decode((int)blockIdx.x + c * (int)gridDim.x);
+            for (int t = 0; t < 2; ++t) {
+                const uint32_t o_tmem = tmem + lane_off + G::kOCol0 + G::kOStride * t;
+                mbar_wait(&bars->o_final[t], c & 1);
+                tc_fence_after();
+                const bool active = (t == 0) || it.two;
+                uint8_t* stg_tile = smem + G::kX0 + t * kRows * G::kStageRow;
+                if (active) {
+                    // the previous store of this staging tile has read its rows (the other tile's
+                    // store, if it is the most recent one, may stay in flight)
+                    if (issuer) {
+                        if (last_t >= 0 && last_t != t) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                        else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    }
+                    asm volatile("bar.sync 11, 128;" ::: "memory");
+                    float o[16];
+                    PAB_TMEM_LD16(o_tmem + 16 * (p.dh / 16), o);  // row sum sits in column dh
+                    tmem_wait_ld();
+                    float l = o[0];
+#pragma unroll
+                    for (int e = 1; e < 16; ++e) l = (e == p.dh % 16) ? o[e] : l;
+                    const float inv = (l > 0.f) ? 1.0f / l : 0.f;
+                    uint8_t* stg = stg_tile + row * (2 * p.dh);  // dense rows: the TMA box layout
+                    for (int cc = 0; 16 * cc < p.dh; ++cc) {
+                        PAB_TMEM_LD16(o_tmem + 16 * cc, o);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < 16; e += 8) {
+                            if (16 * cc + e < p.dh) {
+                                uint32_t w[4];
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) w[q] = pack_bf16(o[e + 2 * q] * inv, o[e + 2 * q + 1] * inv);
+                                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(stg + (16 * cc + e) * 2)),
+                                             "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                                             : "memory");
+                            }
+                        }
+                    }
+                }
+                // O of this tile is in registers / smem: the next item's first P.V may overwrite it
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->o_free[t]);
+                if (active) {
+                    fence_async_smem();  // generic-proxy smem writes -> visible to the TMA (async proxy)
+                    asm volatile("bar.sync 11, 128;" ::: "memory");
+#ifndef PAB_FA_DIAG_EPI_NOSTORE
+                    if (issuer)
+                        asm volatile(
+                            "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];\n\t"
+                            "cp.async.bulk.commit_group;" ::"l"(reinterpret_cast<uint64_t>(&omap)),
+                            "r"(smem_u32(stg_tile)), "r"(0), "r"(it.h), "r"((it.tile0 + t) * kRows), "r"(it.b_idx),
+                            "r"(it.a_idx)
+                            : "memory");
+#endif
+                    last_t = t;
+                }
+            }
+        }
+        if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // tile stores complete before exit
     } else if (warp == kTmaWarp) {
         // ===================================================== TMA producer
         if (lane == 0) {
@@ -873,14 +969,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // tile 0's P.V goes as soon as tile 0's P is stored: its next P store (which
                 // must wait for this P.V) no longer waits behind tile 1's exp section
                 mbar_wait2(&bars->p_full[0], gi & 1, &bars->v_ready[g % 3], (g / 3) & 1);
+                // first P.V of an item overwrites O: the epilogue warps must have read the last item's
+                if (kEpiWarps && j == 0 && c > 0) mbar_wait(&bars->o_free[0], (c - 1) & 1);
                 tc_fence_after();
                 FA_TRACE(lane == 0, gi, 1, 8);
                 issue_pv_tile(g % 3, 0, j > 0, cols_of(j));
                 tc_commit(&bars->o_done[0]);
+                if (kEpiWarps && j == n_kv - 1) tc_commit(&bars->o_final[0]);
                 mbar_wait(&bars->p_full[1], gi & 1);
+                if (kEpiWarps && j == 0 && c > 0) mbar_wait(&bars->o_free[1], (c - 1) & 1);
                 tc_fence_after();
                 if (it.two) issue_pv_tile(g % 3, 1, j > 0, cols_of(j));
                 tc_commit(&bars->o_done[1]);
+                if (kEpiWarps && j == n_kv - 1) tc_commit(&bars->o_final[1]);
             } else {
                 mbar_wait2(&bars->p_full[0], gi & 1, &bars->v_ready[g % 3], (g / 3) & 1);
                 tc_fence_after();
