@@ -153,6 +153,15 @@ int pab_peer_barrier(void* const* flags, void* counter, int rank, int n_w, void*
                      double timeout_s, void* stream);
 
 /*
+ * Redundancy scan on the device: sums of two bf16 site outputs of n elements,
+ * out4 = { sum (a-b)^2, sum a^2, sum b^2, sum a*b } in fp64 (zeroed by the call).
+ * Every metric of the reference's diff_metric (mse, relative_l2, one_minus_cosine;
+ * pkg/src/pab_engine/profiler.py:60-81) follows from them, so redundancy_scan
+ * (profiler.py:140-173) needs no device->host snapshot copies.
+ */
+int pab_diff_sums(const void* a, const void* b, int64_t n, double* out4, void* stream);
+
+/*
  * Fused end-of-step residual drain + classifier-free guidance + DDIM (K8).
  * Replaces: the eps combine and ddim_update of diffusion.sample
  * (pkg/src/pab_engine/diffusion.py:183-189, 100-103).

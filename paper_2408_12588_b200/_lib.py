@@ -75,6 +75,7 @@ SIGNATURES = {
          ctypes.c_double, ctypes.c_double, c_vp],
     ),
     "pab_gelu_bf16": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp]),
+    "pab_diff_sums": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "pab_add_scaled_f32": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_float, c_i64, c_vp]),
     "pab_softmax_rows": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, ctypes.c_float, c_vp]),
     "pab_fill_uniform": (

@@ -612,6 +612,70 @@ extern "C" int pab_add_scaled_f32(float* y, const float* x, const float* w, floa
     return launch_status("add_scaled_f32");
 }
 
+// Redundancy scan on the device (reference profiler.diff_metric / redundancy_scan,
+// pkg/src/pab_engine/profiler.py:60-81, 140-173): the four sums every metric needs,
+// sum (a-b)^2, sum a^2, sum b^2, sum a*b, over two bf16 site outputs, accumulated in
+// fp64 (8 elements per thread in fp32, then fp64 warp / block / grid reductions).
+__global__ void __launch_bounds__(256) diff_sums_kernel(const __nv_bfloat16* __restrict__ a,
+                                                        const __nv_bfloat16* __restrict__ b, int64_t n,
+                                                        double* __restrict__ out) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 8;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8; i < n; i += stride) {
+        float f[4] = {0.f, 0.f, 0.f, 0.f};
+        if (i + 8 <= n) {
+            const uint4 ra = __ldg(reinterpret_cast<const uint4*>(a + i));
+            const uint4 rb = __ldg(reinterpret_cast<const uint4*>(b + i));
+            const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&ra);
+            const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&rb);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float2 x = __bfloat1622float2(ha[j]), y = __bfloat1622float2(hb[j]);
+                f[0] += (x.x - y.x) * (x.x - y.x) + (x.y - y.y) * (x.y - y.y);
+                f[1] += x.x * x.x + x.y * x.y;
+                f[2] += y.x * y.x + y.y * y.y;
+                f[3] += x.x * y.x + x.y * y.y;
+            }
+        } else {
+            for (int64_t k = i; k < n; ++k) {
+                const float x = __bfloat162float(a[k]), y = __bfloat162float(b[k]);
+                f[0] += (x - y) * (x - y);
+                f[1] += x * x;
+                f[2] += y * y;
+                f[3] += x * y;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k] += (double)f[k];
+    }
+    __shared__ double red[8][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][k] = acc[k];
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w][threadIdx.x];
+        atomicAdd(out + threadIdx.x, s);
+    }
+}
+
+extern "C" int pab_diff_sums(const void* a, const void* b, int64_t n, double* out4, void* stream) {
+    if (n < 0) return PAB_ERR_SHAPE;
+    if (!a || !b || !out4) return PAB_ERR_INVALID;
+    if ((uintptr_t)a % 16 || (uintptr_t)b % 16 || (uintptr_t)out4 % 8) return PAB_ERR_UNSUPPORTED;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(out4, 0, 4 * sizeof(double), st) != cudaSuccess) return launch_status("diff_sums memset");
+    if (n == 0) return PAB_OK;
+    int64_t blocks = (n + 256 * 8 - 1) / (256 * 8);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    diff_sums_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(a),
+                                                        reinterpret_cast<const __nv_bfloat16*>(b), n, out4);
+    return launch_status("diff_sums");
+}
+
 extern "C" int pab_gelu_bf16(const void* in, void* out, int64_t n, void* stream) {
     if (n < 0) return PAB_ERR_SHAPE;
     if (n == 0) return PAB_OK;

@@ -287,7 +287,8 @@ class _Step:
 
     def wants_output(self) -> bool:
         """A trace that digests / snapshots site outputs needs o even when it is not cached."""
-        return self.trace is not None and getattr(self.trace, "snapshot_mode", "none") in ("digest", "snapshot")
+        return self.trace is not None and getattr(self.trace, "snapshot_mode", "none") in ("digest", "snapshot",
+                                                                                          "device")
 
     def out_gemm(self, a, w_t, store: bool, token_major: bool = False, rows=None, site=None):
         """Output projection of a computed attention site fused with its residual add: the
@@ -308,7 +309,9 @@ class _Step:
         need = store or self.wants_output()
         o = None
         if need:
-            o = c.cross_slot(site) if site is not None and store else self.out_buffer(store, token_major)
+            # cross sites always land in their zeroed per-site slot, so a traced (uncached) output
+            # also carries the exact zeros of its null-text rows
+            o = c.cross_slot(site) if site is not None else self.out_buffer(store, token_major)
         tm = (c.T, c.S) if token_major else None
         if rows is not None:
             kernels.gemm_residual(a[:rows], w_t, x[:rows], None if o is None else o[:rows], token_major=tm)
