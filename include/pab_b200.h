@@ -274,6 +274,17 @@ int pab_gemm_bf16_residual(const void* A, int64_t lda, const void* B, int64_t ld
                            float* x, int64_t ldx, int64_t M, int64_t N, int64_t K,
                            int64_t tm_t, int64_t tm_s, void* stream);
 
+/*
+ * pab_gemm_bf16_residual that also writes h = bf16(x_new) (row stride ldh, x's
+ * frame-major row order, rows < h_rows only -- h_rows < 0: all; h may be NULL):
+ * the query input of a cross site that
+ * follows the computed site, which the reference forms as x + o then casts
+ * (model.py:376-385, 503) -- the stand-alone cast pass disappears.
+ */
+int pab_gemm_bf16_residual_h(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                             float* x, int64_t ldx, void* h, int64_t ldh, int64_t h_rows, int64_t M, int64_t N,
+                             int64_t K, int64_t tm_t, int64_t tm_s, void* stream);
+
 /* Debug only: record a clock64 event timeline of CTA (0,0,0) of subsequent
  * tcgen05 attention launches into device_buffer (NULL disables). */
 int pab_attn_debug_trace(long long* device_buffer);

@@ -89,6 +89,11 @@ SIGNATURES = {
         ctypes.c_int,
         [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp],
     ),
+    "pab_gemm_bf16_residual_h": (
+        ctypes.c_int,
+        [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64,
+         c_vp],
+    ),
     "pab_attention_select": (ctypes.c_int, [ctypes.POINTER(AttnArgs)]),
     "pab_attn_debug_trace": (ctypes.c_int, [c_vp]),
 }

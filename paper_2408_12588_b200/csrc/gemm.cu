@@ -78,6 +78,10 @@ struct Params {
     int64_t ldx, M, N;
     int64_t tm_t, tm_s;  // > 0: GEMM rows are token-major (b, s, t), x rows frame-major (b, t, s)
     int store_c;
+    // RESID: optional h = bf16(x + o) in x's (frame-major) row order, ld ldh -- the next
+    // cross site's query input, so its stand-alone cast pass (6E bytes) is not needed
+    __nv_bfloat16* h;
+    int64_t ldh, h_rows;  // h rows (x order) < h_rows are written (the live CFG rows of the cross site)
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -328,9 +332,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
             mbar_wait(&bars->xfull[g], xph);
             xph ^= 1;
+            // h row of this thread (x's frame-major order), nullptr if no h output / past M
+            __nv_bfloat16* hrow = nullptr;
+            if (p.h != nullptr) {
+                const int64_t m = (int64_t)row0 + r;
+                if (m < p.M) {
+                    int64_t fr = m;  // (the h_rows check below)
+                    if (p.tm_t > 0) {  // GEMM row (b, s, t) -> stream row (b, t, s)
+                        const int64_t per_b = p.tm_t * p.tm_s, b = m / per_b, rem = m - b * per_b;
+                        const int64_t s_ = rem / p.tm_t, t_ = rem - s_ * p.tm_t;
+                        fr = (b * p.tm_t + t_) * p.tm_s + s_;
+                    }
+                    if (fr < p.h_rows) hrow = p.h + fr * p.ldh + col;
+                }
+            }
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const uint32_t rowaddr = smem_u32(xbuf + h * kXBoxBytes) + (uint32_t)r * 128;
+                uint32_t hp[4];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const uint32_t a = rowaddr + (uint32_t)(((j ^ (r & 7)) * 16));
@@ -339,9 +358,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                  : "=f"(xv.x), "=f"(xv.y), "=f"(xv.z), "=f"(xv.w)
                                  : "r"(a));
                     const float* o = v + 32 * h + 4 * j;
-                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(xv.x + o[0]),
-                                 "f"(xv.y + o[1]), "f"(xv.z + o[2]), "f"(xv.w + o[3])
+                    xv.x += o[0]; xv.y += o[1]; xv.z += o[2]; xv.w += o[3];
+                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(xv.x), "f"(xv.y),
+                                 "f"(xv.z), "f"(xv.w)
                                  : "memory");
+                    hp[2 * (j & 1)] = pack_bf16(xv.x, xv.y);
+                    hp[2 * (j & 1) + 1] = pack_bf16(xv.z, xv.w);
+                    // 8 columns = one 16-byte store; a thread writes whole 128-byte row segments
+                    if ((j & 1) && hrow != nullptr && col + 32 * h + 4 * j + 4 <= p.N)
+                        __stcs(reinterpret_cast<uint4*>(hrow + 32 * h + 4 * (j - 1)),
+                               make_uint4(hp[0], hp[1], hp[2], hp[3]));
                 }
             }
             fence_async_smem();
@@ -467,6 +493,8 @@ static bool map_x4(CUtensorMap* m, float* x, int64_t N, int64_t M, int64_t ldx, 
 struct Resid {
     float* x = nullptr;
     int64_t ldx = 0, tm_t = 0, tm_s = 0;
+    __nv_bfloat16* h = nullptr;
+    int64_t ldh = 0, h_rows = 0;
 };
 
 template <int BN, bool NARROW, bool RESID>
@@ -509,6 +537,9 @@ static int launch_t(const void* A, int64_t lda, const void* B, int64_t ldb, void
     p.tm_t = rs.tm_t;
     p.tm_s = rs.tm_s;
     p.store_c = Cp != nullptr;
+    p.h = rs.h;
+    p.ldh = rs.ldh;
+    p.h_rows = rs.h_rows;
     if (g_sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -566,9 +597,19 @@ extern "C" int pab_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t 
     return dispatch<false>(A, lda, B, ldb, C, ldc, M, N, K, epilogue, Resid{}, reinterpret_cast<cudaStream_t>(stream));
 }
 
+extern "C" int pab_gemm_bf16_residual_h(const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
+                                        int64_t ldc, float* x, int64_t ldx, void* h, int64_t ldh, int64_t h_rows,
+                                        int64_t M, int64_t N, int64_t K, int64_t tm_t, int64_t tm_s, void* stream);
+
 extern "C" int pab_gemm_bf16_residual(const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
                                       int64_t ldc, float* x, int64_t ldx, int64_t M, int64_t N, int64_t K,
                                       int64_t tm_t, int64_t tm_s, void* stream) {
+    return pab_gemm_bf16_residual_h(A, lda, B, ldb, C, ldc, x, ldx, nullptr, 0, 0, M, N, K, tm_t, tm_s, stream);
+}
+
+extern "C" int pab_gemm_bf16_residual_h(const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
+                                        int64_t ldc, float* x, int64_t ldx, void* h, int64_t ldh, int64_t h_rows,
+                                        int64_t M, int64_t N, int64_t K, int64_t tm_t, int64_t tm_s, void* stream) {
     using namespace pab::gemm;
     if (M == 0) return PAB_OK;
     const int st = check_args(A, lda, B, ldb, C, ldc, M, N, K);
@@ -578,9 +619,13 @@ extern "C" int pab_gemm_bf16_residual(const void* A, int64_t lda, const void* B,
     if (tm_t < 0 || tm_s < 0 || (tm_t > 0) != (tm_s > 0) || (tm_t > 0 && M % (tm_t * tm_s))) return PAB_ERR_SHAPE;
     // token-major rows: every 128-row block must be whole tokens of one batch entry
     if (tm_t > 0 && (128 % tm_t || (tm_t * tm_s) % 128)) return PAB_ERR_UNSUPPORTED;
+    if (h && (ldh < N || (uintptr_t)h % 16 || ldh % 8 || N % 8)) return PAB_ERR_UNSUPPORTED;
     Resid rs;
     rs.x = x;
     rs.ldx = ldx;
+    rs.h = reinterpret_cast<__nv_bfloat16*>(h);
+    rs.ldh = ldh;
+    rs.h_rows = h ? (h_rows < 0 || h_rows > M ? M : h_rows) : 0;
     rs.tm_t = tm_t;
     rs.tm_s = tm_s;
     return dispatch<true>(A, lda, B, ldb, C, ldc, M, N, K, 2, rs, reinterpret_cast<cudaStream_t>(stream));

@@ -234,10 +234,13 @@ def residual_token_major_ok(T: int, S: int) -> bool:
     return 128 % T == 0 and (T * S) % 128 == 0
 
 
-def gemm_residual(a: torch.Tensor, w_t: torch.Tensor, x: torch.Tensor, out=None, token_major=None):
+def gemm_residual(a: torch.Tensor, w_t: torch.Tensor, x: torch.Tensor, out=None, token_major=None, h=None,
+                  h_rows=-1):
     """x[perm(m)] += bf16(a @ w_t^T)[m] (fp32 residual stream, in place) and, when ``out`` is
     given, out = bf16(a @ w_t^T) (the cached site output).  token_major = (T, S): the rows
-    of ``a`` are (b, s, t), the rows of ``x`` (b, t, s)."""
+    of ``a`` are (b, s, t), the rows of ``x`` (b, t, s).  ``h`` (bf16, x's shape and row
+    order): also h = bf16(x_new) for x rows < ``h_rows`` (-1: all), the next cross site's
+    query input."""
     lib = _lib.load()
     for t, name in ((a, "A"), (w_t, "B")):
         _need(t, torch.bfloat16, name)
@@ -254,10 +257,17 @@ def gemm_residual(a: torch.Tensor, w_t: torch.Tensor, x: torch.Tensor, out=None,
         if out.shape != (M, N) or out.stride(1) != 1:
             raise ShapeError("gemm_residual output must be (M, N) with unit column stride")
     tm_t, tm_s = token_major if token_major is not None else (0, 0)
-    _lib.check(lib.pab_gemm_bf16_residual(a.data_ptr(), a.stride(0), w_t.data_ptr(), w_t.stride(0),
-                                          out.data_ptr() if out is not None else None,
-                                          out.stride(0) if out is not None else 0, x2.data_ptr(), x2.stride(0),
-                                          M, N, K, int(tm_t), int(tm_s), _stream()), "pab_gemm_bf16_residual")
+    if h is not None:
+        _need(h, torch.bfloat16, "h")
+        h2 = h.view(-1, h.shape[-1])
+        if h2.shape != (M, N) or h2.stride(1) != 1:
+            raise ShapeError("gemm_residual h must match the residual stream")
+    _lib.check(lib.pab_gemm_bf16_residual_h(a.data_ptr(), a.stride(0), w_t.data_ptr(), w_t.stride(0),
+                                            out.data_ptr() if out is not None else None,
+                                            out.stride(0) if out is not None else 0, x2.data_ptr(), x2.stride(0),
+                                            h2.data_ptr() if h is not None else None,
+                                            h2.stride(0) if h is not None else 0, int(h_rows),
+                                            M, N, K, int(tm_t), int(tm_s), _stream()), "pab_gemm_bf16_residual_h")
     return out
 
 

@@ -57,6 +57,11 @@ SP, TM, CR, ML = ComponentKind.SPATIAL, ComponentKind.TEMPORAL, ComponentKind.CR
 torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = False
 
 
+# A/B switch for measurements: PAB_FUSED_CAST=0 forms the cross query input with the
+# stand-alone cast prologue instead of the preceding O GEMM's epilogue
+_FUSED_CAST = os.environ.get("PAB_FUSED_CAST", "1") != "0"
+
+
 @dataclass
 class Launches:
     """Per-step accounting of what ran (decision log + kernel counts)."""
@@ -65,6 +70,7 @@ class Launches:
     sites_reused: int = 0
     attention_calls: int = 0
     prologue_calls: int = 0
+    prologues_fused: int = 0  # cross-site cast passes produced by the preceding O GEMM instead
     gemm_calls: int = 0
     other_calls: int = 0
     log: list = field(default_factory=list)  # (step, layer, kind, block, decision, source)
@@ -243,6 +249,10 @@ class _Step:
         self.src, self.r = z, r
         self.decisions, self.cache, self.trace = decisions, cache, trace
         self.pending: list = []
+        # c.h == bf16(r) with nothing pending: written by the O GEMM of a computed site whose next
+        # site is a computing cross site (its query input), which then skips its cast prologue
+        self.h_cast = False
+        self.emit_h = False  # the next out_gemm should produce that h
         self.sink = _Sink(flop_sink, ctx)
         self.mods = ctx.mods[step]
 
@@ -258,6 +268,7 @@ class _Step:
         c.launches.prologue_calls += 1
         self.src = self.r
         self.pending = []
+        self.h_cast = False
 
     def flush(self):
         """Materialise the residual stream (no normalised output)."""
@@ -316,7 +327,11 @@ class _Step:
         if rows is not None:
             kernels.gemm_residual(a[:rows], w_t, x[:rows], None if o is None else o[:rows], token_major=tm)
         else:
-            kernels.gemm_residual(a, w_t, x, o, token_major=tm)
+            emit = self.emit_h and not self.pending and self.src is self.r
+            kernels.gemm_residual(a, w_t, x, o, token_major=tm, h=c.h if emit else None,
+                                  h_rows=c.cross_live * c.T * c.S)
+            self.h_cast = emit
+        self.emit_h = False
         self.added = True
         return o
 
@@ -461,7 +476,12 @@ class _Step:
         c = self.ctx
 
         def compute(store):
-            self.prologue(2)
+            if self.h_cast and not self.pending and self.src is self.r:
+                # the previous site's O GEMM already wrote h = bf16(x) (its residual epilogue)
+                self.h_cast = False
+                c.launches.prologues_fused += 1
+            else:
+                self.prologue(2)
             rl = c.cross_live * c.T * c.S  # rows with non-null text (see StepContext.build)
             if rl == 0:  # every row null: the output is exactly 0, nothing to add
                 self.added = True
@@ -514,6 +534,8 @@ class _Step:
             self.flush()
             x_in = self.ctx.delta_in(self.r)
         sc = self.ctx.broadcast_object == "scores"
+        live = self.ctx.cross_live > 0 and _FUSED_CAST
+        self.emit_h = live and not sc and d.source(li, CR) == self.step  # spatial O GEMM -> cross q input
         self.run_site(li, SP, "s", self.attn_site(lp.spatial, MOD_SPATIAL, False),
                       scores=self.attn_scores(lp.spatial, MOD_SPATIAL, False) if sc else None)
         self.run_site(li, CR, "s", self.cross_site(lp.cross_spatial, 0),
@@ -522,6 +544,7 @@ class _Step:
         if temporal_hook is not None:
             temporal_hook(self, li, lp)
         else:
+            self.emit_h = live and not sc and self.ctx.cfg.cross_in_temporal and d.source(li, CR) == self.step
             self.run_site(li, TM, "t", self.attn_site(lp.temporal, MOD_TEMPORAL, True), token_major=True,
                           scores=self.attn_scores(lp.temporal, MOD_TEMPORAL, True) if sc else None)
         if self.ctx.cfg.cross_in_temporal:

@@ -81,3 +81,23 @@ def test_gemm_residual_epilogue(M, N, K, store, tm):
         T, S = tm
         o_rows = o_rows.view(-1, S, T, N).permute(0, 2, 1, 3).reshape(M, N)
     assert torch.equal(x, x0 + o_rows)
+
+
+@pytest.mark.parametrize("M,N,K,store,tm,h_rows", [(49920, 1152, 1152, True, None, 24960),
+                                                   (49920, 1152, 1152, False, (16, 1560), -1),
+                                                   (4096, 1152, 1152, False, (16, 128), 2048),
+                                                   (300, 144, 576, False, None, -1)])
+def test_gemm_residual_h_output(M, N, K, store, tm, h_rows):
+    """The residual epilogue's h = bf16(x + o) output (the next cross site's query input):
+    bitwise bf16 of the updated stream, in the stream's frame-major row order, only rows
+    < h_rows written (the live CFG rows)."""
+    g = torch.Generator(device="cuda").manual_seed(2)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    w_t = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    x = torch.randn(M, N, device="cuda", generator=g)
+    h = torch.full((M, N), 7.0, device="cuda", dtype=torch.bfloat16)
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16) if store else None
+    kernels.gemm_residual(a, w_t, x, out, token_major=tm, h=h, h_rows=h_rows)
+    lim = M if h_rows < 0 else h_rows
+    assert torch.equal(h[:lim], x[:lim].to(torch.bfloat16))
+    assert bool((h[lim:] == 7.0).all())
