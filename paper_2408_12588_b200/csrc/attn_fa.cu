@@ -599,6 +599,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     m4[g] = (kG % 2 == 0) ? fmaxf(m, s[kG * g + kG - 1]) : m;
                 }
                 float mx = max3(fmaxf(m4[0], m4[1]), m4[2], m4[3]);
+#ifdef PAB_FA_DIAG_NOMAX  // timing diagnostic only: row max of the first tile reused (wrong results)
+                if (j > 0) mx = s[0];
+#endif
                 if (kSplit > 1) {
                     float* xs = xch + ((it_n & 1) * 2 + t) * 2 * kRows;
                     xs[hc * kRows + row] = mx;
