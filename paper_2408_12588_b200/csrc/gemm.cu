@@ -44,13 +44,17 @@ constexpr int kStageBoxBytes = kRowsCta * 128;  // 128 rows x 64 bf16 epilogue b
 static_assert(kEpiWarps == 4 || kEpiWarps == 8, "epilogue warps");
 
 constexpr int kXBoxBytes = kRowsCta * 128;   // 128 rows x 32 fp32 residual box
-template <int BN, bool RESID = false>
+// RESID: 0 plain epilogue; 1 residual add with the fp32 x chunk streamed through smem by TMA
+// (epilogue latency matters: K = 1152 projections); 2 residual add by direct per-thread
+// global read-modify-write of whole row segments -- no smem, so the operand ring keeps its
+// depth (K = 4608: the MLP w2 GEMM, whose epilogue hides behind a long mainloop)
+template <int BN, int RESID = 0>
 struct Cfg {
     static constexpr int kABytes = kRowsCta * kBK * 2;          // 16 KB
     static constexpr int kBBytes = (BN / 2) * kBK * 2;          // BN/2 rows of B
     static constexpr int kStageBytes = kABytes + kBBytes;
     // RESID: per epilogue group, one 64-column fp32 residual chunk (two 32-column boxes)
-    static constexpr int kXBytes = RESID ? kEpiGroups * 2 * kXBoxBytes : 0;
+    static constexpr int kXBytes = RESID == 1 ? kEpiGroups * 2 * kXBoxBytes : 0;
     static constexpr int kEpiBytes = kEpiGroups * kBufPerGroup * kStageBoxBytes + kXBytes;
     static constexpr int kStages = (232448 - kEpiBytes - 1280) / kStageBytes > 8
                                        ? 8 : (232448 - kEpiBytes - 1280) / kStageBytes;
@@ -162,7 +166,7 @@ __device__ __forceinline__ void tile_coords(int t, const Params& p, int& m, int&
     n = r / gm;
 }
 
-template <int BN, bool NARROW, bool RESID>
+template <int BN, bool NARROW, int RESID>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_x,
@@ -193,7 +197,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         prefetch_map(&map_a);
         prefetch_map(&map_b);
         prefetch_map(&map_c);
-        if (RESID) prefetch_map(&map_x);
+        if (RESID == 1) prefetch_map(&map_x);
     }
     if (warp == kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
@@ -390,7 +394,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tile_coords(t, p, tm, tn);
             const int row0 = tm * 2 * kRowsCta + (int)rank * kRowsCta;
             const int kChunks = ((NARROW && tn == p.n_tiles - 1) ? p.n_last : BN) / 64;
-            if constexpr (RESID) {
+            if constexpr (RESID == 1) {
                 if (r == 0 && g < kChunks) x_load(tn * BN + g * 64, row0);  // before the accumulator is ready
             }
             mbar_wait(&bars->tfull[acc], aph);
@@ -412,9 +416,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int i = 0; i < 64; ++i) v[i] = gelu_tanh(v[i]);
                 }
-                if constexpr (RESID) {
+                if constexpr (RESID == 1) {
                     resid_chunk(v, tn * BN + c * 64, row0, c + kEpiGroups < kChunks ? tn * BN + (c + kEpiGroups) * 64 : -1);
                     continue;
+                }
+                if constexpr (RESID == 2) {
+                    // x[row] += bf16(o): this thread's row segment of 64 fp32 (256 contiguous bytes),
+                    // streamed (each byte touched once); rows >= M and columns >= N skipped
+#pragma unroll
+                    for (int i = 0; i < 64; ++i) v[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
+                    const int64_t m = (int64_t)row0 + r;
+                    const int col = tn * BN + c * 64;
+                    if (m < p.M) {
+                        float4* xr = reinterpret_cast<float4*>(p.x + m * p.ldx + col);
+#pragma unroll
+                        for (int q0 = 0; q0 < 16; q0 += 4) {
+                            float4 xv[4];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                if (col + 4 * (q0 + q) < p.N) xv[q] = __ldcs(xr + q0 + q);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const float* o = v + 4 * (q0 + q);
+                                xv[q].x += o[0]; xv[q].y += o[1]; xv[q].z += o[2]; xv[q].w += o[3];
+                                if (col + 4 * (q0 + q) < p.N) __stcs(xr + q0 + q, xv[q]);
+                            }
+                        }
+                    }
+                    if (!p.store_c) continue;  // o itself only when the site is cached
                 }
                 uint8_t* sb = stage0 + box * kStageBoxBytes;
                 // the TMA store issued from this buffer kBufPerGroup boxes ago must have read it
@@ -468,6 +497,7 @@ static int env_int(const char* name, int dflt) {
     return v ? atoi(v) : dflt;
 }
 static int g_group = env_int("PAB_GEMM_GROUP", 8);
+static int g_direct_k = env_int("PAB_GEMM_RESID_DIRECT_K", 2048);  // K from which RESID == 2 is used
 
 static bool map_x4(CUtensorMap* m, float* x, int64_t N, int64_t M, int64_t ldx, int64_t tm_t, int64_t tm_s) {
     auto encode = get_encode();
@@ -497,7 +527,7 @@ struct Resid {
     int64_t ldh = 0, h_rows = 0;
 };
 
-template <int BN, bool NARROW, bool RESID>
+template <int BN, bool NARROW, int RESID>
 static int launch_t(const void* A, int64_t lda, const void* B, int64_t ldb, void* Cp, int64_t ldc, int64_t M,
                     int64_t N, int64_t K, int epilogue, const Resid& rs, cudaStream_t st) {
     using C = Cfg<BN, RESID>;
@@ -515,7 +545,7 @@ static int launch_t(const void* A, int64_t lda, const void* B, int64_t ldb, void
     if (!map_2d(&ma, A, K, M, lda, kBK, kRowsCta) || !map_2d(&mb, B, K, N, ldb, kBK, BN / 2) ||
         !map_2d(&mc, cbase, Cp ? N : K, M, cld, 64, kRowsCta))
         return PAB_ERR_CUDA;
-    if (RESID) {
+    if (RESID == 1) {
         if (!map_x4(&mx, rs.x, N, M, rs.ldx, rs.tm_t, rs.tm_s)) return PAB_ERR_CUDA;
     } else {
         mx = ma;  // unused
@@ -551,14 +581,14 @@ static int launch_t(const void* A, int64_t lda, const void* B, int64_t ldb, void
     return launch_status("gemm");
 }
 
-template <int BN, bool RESID>
+template <int BN, int RESID>
 static int launch(const void* A, int64_t lda, const void* B, int64_t ldb, void* Cp, int64_t ldc, int64_t M,
                   int64_t N, int64_t K, int epilogue, const Resid& rs, cudaStream_t st) {
     return (N % BN) ? launch_t<BN, true, RESID>(A, lda, B, ldb, Cp, ldc, M, N, K, epilogue, rs, st)
                     : launch_t<BN, false, RESID>(A, lda, B, ldb, Cp, ldc, M, N, K, epilogue, rs, st);
 }
 
-template <bool RESID>
+template <int RESID>
 static int dispatch(const void* A, int64_t lda, const void* B, int64_t ldb, void* Cp, int64_t ldc, int64_t M,
                     int64_t N, int64_t K, int epilogue, const Resid& rs, cudaStream_t st) {
     // 256-wide tiles read the least shared memory per MMA (192: -6%, 128: -25% at N = 3456 / 4608,
@@ -594,7 +624,7 @@ extern "C" int pab_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t 
     const int st = check_args(A, lda, B, ldb, C, ldc, M, N, K);
     if (st != PAB_OK) return st;
     if (epilogue != 0 && epilogue != 1) return PAB_ERR_INVALID;
-    return dispatch<false>(A, lda, B, ldb, C, ldc, M, N, K, epilogue, Resid{}, reinterpret_cast<cudaStream_t>(stream));
+    return dispatch<0>(A, lda, B, ldb, C, ldc, M, N, K, epilogue, Resid{}, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int pab_gemm_bf16_residual_h(const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
@@ -628,5 +658,8 @@ extern "C" int pab_gemm_bf16_residual_h(const void* A, int64_t lda, const void* 
     rs.h_rows = h ? (h_rows < 0 || h_rows > M ? M : h_rows) : 0;
     rs.tm_t = tm_t;
     rs.tm_s = tm_s;
-    return dispatch<true>(A, lda, B, ldb, C, ldc, M, N, K, 2, rs, reinterpret_cast<cudaStream_t>(stream));
+    // deep-K GEMMs (the MLP w2) take the direct read-modify-write epilogue (frame-major rows, no h)
+    if (K >= g_direct_k && tm_t == 0 && h == nullptr)
+        return dispatch<2>(A, lda, B, ldb, C, ldc, M, N, K, 2, rs, reinterpret_cast<cudaStream_t>(stream));
+    return dispatch<1>(A, lda, B, ldb, C, ldc, M, N, K, 2, rs, reinterpret_cast<cudaStream_t>(stream));
 }

@@ -60,6 +60,8 @@ torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = False
 # A/B switch for measurements: PAB_FUSED_CAST=0 forms the cross query input with the
 # stand-alone cast prologue instead of the preceding O GEMM's epilogue
 _FUSED_CAST = os.environ.get("PAB_FUSED_CAST", "1") != "0"
+# PAB_W2_RESID=0: the MLP's w2 GEMM writes o and the next prologue adds it (A/B switch)
+_W2_RESID = os.environ.get("PAB_W2_RESID", "1") != "0"
 
 
 @dataclass
@@ -503,9 +505,17 @@ class _Step:
             # w1 GEMM with the tanh-GELU applied in its epilogue (no extra HBM pass over
             # the 4D-wide hidden activation), then w2; the next prologue adds o
             kernels.gemm(c.h, p.w1_t, c.hidden, kernels.EPI_GELU)
+            c.launches.gemm_calls += 2
+            if _W2_RESID:
+                # w2 with the residual add in its epilogue (direct read-modify-write at K = 4D):
+                # r += o here, o written only when cached / traced
+                x = self.r.view(-1, c.D)
+                o = self.out_buffer(store) if (store or self.wants_output()) else None
+                kernels.gemm_residual(c.hidden, p.w2_t, x, o)
+                self.added = True
+                return o
             o = self.out_buffer(store)
             kernels.gemm(c.hidden, p.w2_t, o)
-            c.launches.gemm_calls += 2
             return o
 
         return compute

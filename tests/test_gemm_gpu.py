@@ -61,10 +61,13 @@ def test_gemm_strided_operands():
 
 @pytest.mark.parametrize("M,N,K,store,tm", [(49920, 1152, 4608, False, None), (49920, 1152, 1152, True, None),
                                             (4096, 1152, 1152, True, (16, 256)), (300, 144, 576, True, None),
-                                            (2048, 144, 144, False, (8, 128)), (24960, 1152, 1152, False, None)])
+                                            (2048, 144, 144, False, (8, 128)), (24960, 1152, 1152, False, None),
+                                            (49920, 1152, 4608, True, None), (300, 144, 4608, True, None),
+                                            (1000, 1152, 2304, False, None)])
 def test_gemm_residual_epilogue(M, N, K, store, tm):
     """x[perm(m)] += bf16(A B^T)[m] in the epilogue (the site output's residual add), with and
-    without the cached-output store, frame- and token-major rows."""
+    without the cached-output store, frame- and token-major rows; K >= 2048 takes the direct
+    read-modify-write epilogue (the MLP w2), with ragged M and N."""
     g = torch.Generator(device="cuda").manual_seed(1)
     a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
     w_t = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
