@@ -421,29 +421,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     continue;
                 }
                 if constexpr (RESID == 2) {
-                    // x[row] += bf16(o): this thread's row segment of 64 fp32 (256 contiguous bytes),
-                    // streamed (each byte touched once); rows >= M and columns >= N skipped
+                    // x += bf16(o) by the whole group, coalesced: o goes through this group's bf16
+                    // staging box (the layout of the C store), then each warp instruction reads and
+                    // writes 4 full 256-byte x row segments (8 columns per thread); the box also
+                    // feeds the o store when the site is cached.  No extra smem.
+                    uint8_t* sb = stage0 + box * kStageBoxBytes;
+                    if (r == 0) bulk_wait_read<kBufPerGroup - 1>();
+                    named_bar(1 + g, 128);
+                    const uint32_t rowaddr = smem_u32(sb) + (uint32_t)r * 128;
 #pragma unroll
-                    for (int i = 0; i < 64; ++i) v[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
-                    const int64_t m = (int64_t)row0 + r;
+                    for (int j = 0; j < 8; ++j)
+                        st_shared_v4(rowaddr + (uint32_t)(((j ^ (r & 7)) * 16)), pack_bf16(v[8 * j], v[8 * j + 1]),
+                                     pack_bf16(v[8 * j + 2], v[8 * j + 3]), pack_bf16(v[8 * j + 4], v[8 * j + 5]),
+                                     pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+                    fence_async_smem();
+                    named_bar(1 + g, 128);
                     const int col = tn * BN + c * 64;
-                    if (m < p.M) {
-                        float4* xr = reinterpret_cast<float4*>(p.x + m * p.ldx + col);
-#pragma unroll
-                        for (int q0 = 0; q0 < 16; q0 += 4) {
-                            float4 xv[4];
-#pragma unroll
-                            for (int q = 0; q < 4; ++q)
-                                if (col + 4 * (q0 + q) < p.N) xv[q] = __ldcs(xr + q0 + q);
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                const float* o = v + 4 * (q0 + q);
-                                xv[q].x += o[0]; xv[q].y += o[1]; xv[q].z += o[2]; xv[q].w += o[3];
-                                if (col + 4 * (q0 + q) < p.N) __stcs(xr + q0 + q, xv[q]);
-                            }
-                        }
+                    if (r == 0 && p.store_c) {
+                        tma_store_2d(&map_c, sb, col, row0);
+                        bulk_commit();
                     }
-                    if (!p.store_c) continue;  // o itself only when the site is cached
+#pragma unroll 2
+                    for (int it = 0; it < 8; ++it) {
+                        const int idx = it * 128 + r, rr = idx >> 3, seg = idx & 7;
+                        const int64_t m = (int64_t)row0 + rr;
+                        if (m >= p.M || col + 8 * seg >= p.N) continue;
+                        uint32_t w[4];
+                        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                                     : "r"(smem_u32(sb) + (uint32_t)rr * 128 + (uint32_t)((seg ^ (rr & 7)) * 16)));
+                        float4* xr = reinterpret_cast<float4*>(p.x + m * p.ldx + col + 8 * seg);
+                        float4 a = __ldcs(xr), b = __ldcs(xr + 1);
+                        const float2 o0 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w[0]));
+                        const float2 o1 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w[1]));
+                        const float2 o2 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w[2]));
+                        const float2 o3 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w[3]));
+                        a.x += o0.x; a.y += o0.y; a.z += o1.x; a.w += o1.y;
+                        b.x += o2.x; b.y += o2.y; b.z += o3.x; b.w += o3.y;
+                        __stcs(xr, a);
+                        __stcs(xr + 1, b);
+                    }
+                    if (++box == kBufPerGroup) box = 0;
+                    continue;
                 }
                 uint8_t* sb = stage0 + box * kStageBoxBytes;
                 // the TMA store issued from this buffer kBufPerGroup boxes ago must have read it
@@ -659,7 +678,7 @@ extern "C" int pab_gemm_bf16_residual_h(const void* A, int64_t lda, const void* 
     rs.tm_t = tm_t;
     rs.tm_s = tm_s;
     // deep-K GEMMs (the MLP w2) take the direct read-modify-write epilogue (frame-major rows, no h)
-    if (K >= g_direct_k && tm_t == 0 && h == nullptr)
+    if (K >= g_direct_k && tm_t == 0 && h == nullptr && N % 8 == 0 && ldx % 8 == 0)
         return dispatch<2>(A, lda, B, ldb, C, ldc, M, N, K, 2, rs, reinterpret_cast<cudaStream_t>(stream));
     return dispatch<1>(A, lda, B, ldb, C, ldc, M, N, K, 2, rs, reinterpret_cast<cudaStream_t>(stream));
 }

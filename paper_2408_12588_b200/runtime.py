@@ -60,8 +60,10 @@ torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = False
 # A/B switch for measurements: PAB_FUSED_CAST=0 forms the cross query input with the
 # stand-alone cast prologue instead of the preceding O GEMM's epilogue
 _FUSED_CAST = os.environ.get("PAB_FUSED_CAST", "1") != "0"
-# PAB_W2_RESID=0: the MLP's w2 GEMM writes o and the next prologue adds it (A/B switch)
-_W2_RESID = os.environ.get("PAB_W2_RESID", "1") != "0"
+# PAB_W2_RESID=1: the MLP's w2 GEMM adds o to the residual in its epilogue (coalesced group
+# read-modify-write, no extra smem) instead of the next prologue -- measured neutral on C3
+# (w2 0.378 -> 0.405 ms vs a 6E-lighter prologue; 3.048-3.058 s/video both ways), off by default
+_W2_RESID = os.environ.get("PAB_W2_RESID", "0") == "1"
 
 
 @dataclass
