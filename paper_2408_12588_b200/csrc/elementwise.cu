@@ -283,22 +283,10 @@ static int launch_modnorm_vec(const float* x_in, float* x_out, const PendingList
 // --------------------------------------------------------------------------
 // K8: end-of-step drain + CFG + DDIM (diffusion.py:100-103, 183-189)
 // --------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) ddim_cfg_kernel(
-    float* __restrict__ z, const float* __restrict__ r, PendingList pend, int batch,
-    int64_t n, int guidance, float g, float c_noise, float c_signal, float c_next_sig,
-    float c_next_noise) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    float eps[8];
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-        if (b >= batch) break;
-        float e = r[(int64_t)b * n + i];
-#pragma unroll
-        for (int p = 0; p < PAB_MAX_PENDING; ++p)
-            if (p < pend.n) e = __fadd_rn(e, __bfloat162float(pend.p[p][(int64_t)b * n + i]));
-        eps[b] = e;
-    }
+// the per-element fp32 op sequence of numpy (eps accumulation in order, CFG, DDIM)
+__device__ __forceinline__ void ddim_cfg_elem(float* eps, const float* zin, float* zout, int batch, int guidance,
+                                              float g, float c_noise, float c_signal, float c_next_sig,
+                                              float c_next_noise) {
     if (guidance) {
         // eps_u + g * (eps_c - eps_u), conditional half first (diffusion.py:183-186)
         const float eh = __fadd_rn(eps[1], __fmul_rn(g, __fsub_rn(eps[0], eps[1])));
@@ -308,9 +296,58 @@ __global__ void __launch_bounds__(256) ddim_cfg_kernel(
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
         if (b >= batch) break;
+        const float x0 = __fdiv_rn(__fsub_rn(zin[b], __fmul_rn(c_noise, eps[b])), c_signal);
+        zout[b] = __fadd_rn(__fmul_rn(c_next_sig, x0), __fmul_rn(c_next_noise, eps[b]));
+    }
+}
+
+// VEC consecutive elements per thread (4: one float4 of z / r and 8 bytes of each bf16
+// pending term per batch row; 1: scalar, for unaligned or ragged n)
+template <int VEC>
+__global__ void __launch_bounds__(256) ddim_cfg_kernel(
+    float* __restrict__ z, const float* __restrict__ r, PendingList pend, int batch,
+    int64_t n, int guidance, float g, float c_noise, float c_signal, float c_next_sig,
+    float c_next_noise) {
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * VEC;
+    if (i >= n) return;
+    float eps[VEC][8], zv[VEC][8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        if (b >= batch) break;
         const int64_t k = (int64_t)b * n + i;
-        const float x0 = __fdiv_rn(__fsub_rn(z[k], __fmul_rn(c_noise, eps[b])), c_signal);
-        z[k] = __fadd_rn(__fmul_rn(c_next_sig, x0), __fmul_rn(c_next_noise, eps[b]));
+        float rv[VEC], zz[VEC];
+        VecT<VEC>::load_f32(r + k, rv);
+        VecT<VEC>::load_f32(z + k, zz);
+#pragma unroll
+        for (int p = 0; p < PAB_MAX_PENDING; ++p) {
+            if (p < pend.n) {
+                float o[VEC] = {};
+                VecT<VEC>::add_bf16(pend.p[p] + k, o);
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) rv[e] = __fadd_rn(rv[e], o[e]);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+            eps[e][b] = rv[e];
+            zv[e][b] = zz[e];
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+        float out[8];
+        ddim_cfg_elem(eps[e], zv[e], out, batch, guidance, g, c_noise, c_signal, c_next_sig, c_next_noise);
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+            if (b < batch) zv[e][b] = out[b];
+    }
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        if (b >= batch) break;
+        float zz[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) zz[e] = zv[e][b];
+        VecT<VEC>::store_f32(z + (int64_t)b * n + i, zz);
     }
 }
 
@@ -543,9 +580,18 @@ extern "C" int pab_ddim_cfg(float* z, const float* r, const void* const* pending
     PendingList pl = make_pending(pending, n_pending);
     const float c_noise = (float)sqrt(1.0 - a_cur), c_signal = (float)sqrt(a_cur);
     const float c_next_sig = (float)sqrt(a_next), c_next_noise = (float)sqrt(1.0 - a_next);
-    dim3 block(256), grid((unsigned)((n + 255) / 256));
-    ddim_cfg_kernel<<<grid, block, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-        z, r, pl, batch, n, guidance, (float)guidance_scale, c_noise, c_signal, c_next_sig, c_next_noise);
+    bool vec = n % 4 == 0 && (uintptr_t)z % 16 == 0 && (uintptr_t)r % 16 == 0;
+    for (int i = 0; i < n_pending; ++i) vec = vec && (uintptr_t)pending[i] % 8 == 0;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (vec) {
+        dim3 block(256), grid((unsigned)((n / 4 + 255) / 256));
+        ddim_cfg_kernel<4><<<grid, block, 0, st>>>(z, r, pl, batch, n, guidance, (float)guidance_scale, c_noise,
+                                                    c_signal, c_next_sig, c_next_noise);
+    } else {
+        dim3 block(256), grid((unsigned)((n + 255) / 256));
+        ddim_cfg_kernel<1><<<grid, block, 0, st>>>(z, r, pl, batch, n, guidance, (float)guidance_scale, c_noise,
+                                                    c_signal, c_next_sig, c_next_noise);
+    }
     return launch_status("ddim_cfg");
 }
 

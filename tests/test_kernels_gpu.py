@@ -213,9 +213,10 @@ def test_residual_modnorm(D, n_pending, mode):
 
 
 @pytest.mark.parametrize("guidance", [False, True])
-def test_ddim_cfg_exact(guidance):
+@pytest.mark.parametrize("n", [4097, 4096 * 3])
+def test_ddim_cfg_exact(guidance, n):
+    """bit-exact with numpy's fp32 sequence: scalar path (ragged n) and float4 path"""
     B = 2 if guidance else 1
-    n = 4097
     z = torch.randn(B, n, device=DEV)
     r = torch.randn(B, n, device=DEV)
     pend = [torch.randn(B, n, device=DEV).to(torch.bfloat16) for _ in range(2)]
