@@ -486,6 +486,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     io_bytes = x_dev.numel() * x_dev.element_size()  # this rank's share of the latent, each way
+    if getattr(den, "hook", None) is not None and den.hook.px is not None:
+        den.hook.px.check()  # a timed-out peer barrier would make the timings meaningless
 
     # all-to-all traffic of one video: calls and bytes from the run's
     # ledger, the per-call time from the same exchange timed alone (CUDA events, max over ranks)
