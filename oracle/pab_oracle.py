@@ -137,9 +137,26 @@ def _softmax(z):
     return e / e.sum(-1, keepdims=True)
 
 
+_SCORE_CHUNK_BYTES = 1 << 31  # fp32 logits materialised at once (C5 spatial: 53 GB unchunked)
+
+
 def attention(q, k, v, rb=None):
     """softmax(q k^T / sqrt(dh)) v over the last two axes (numerics.py:133-151).
-    rb: bf16 rounding of the unnormalised probabilities (emulation mode)."""
+    rb: bf16 rounding of the unnormalised probabilities (emulation mode).  Large
+    problems are evaluated in chunks of the leading (batch, frame, head) axes; every
+    chunk is the same per-problem computation, so the result does not depend on it."""
+    lead = q.shape[:-2]
+    nq, nk = q.shape[-2], k.shape[-2]
+    n = int(np.prod(lead)) if lead else 1
+    per = max(1, _SCORE_CHUNK_BYTES // max(1, nq * nk * 4))
+    if n > per and lead:
+        q2 = q.reshape(n, nq, q.shape[-1])
+        k2 = np.broadcast_to(k, lead + k.shape[-2:]).reshape(n, nk, k.shape[-1])
+        v2 = np.broadcast_to(v, lead + v.shape[-2:]).reshape(n, nk, v.shape[-1])
+        out = np.empty((n, nq, v.shape[-1]), dtype=np.result_type(q, v))
+        for i in range(0, n, per):
+            out[i:i + per] = attention(q2[i:i + per], k2[i:i + per], v2[i:i + per], rb)
+        return out.reshape(lead + (nq, v.shape[-1]))
     s = np.matmul(q, np.swapaxes(k, -1, -2)) * np.float32(1.0 / math.sqrt(q.shape[-1]))
     if rb is None:
         return np.matmul(_softmax(s), v)

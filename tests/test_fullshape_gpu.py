@@ -1,8 +1,9 @@
 """Full-size parity slices: one layer of the C2/C3/C4 blocks at
 their real shapes (D1152, H16, T16, S1024/1560, M120/300, CFG batch 2) for a few
 denoising steps whose tables broadcast sites, against the CPU oracle; a 4-layer
-x 30-step C3 run against an oracle fixture (tests/golden/c3_deep.npz); and C5's
-3600-token spatial attention at op level against a torch fp32 reference."""
+x 30-step C3 run against an oracle fixture (tests/golden/c3_deep.npz); a C5 layer
+(T32, S3600) for two steps; and C5's 3600-token spatial attention at op level against
+a torch fp32 reference."""
 
 import numpy as np
 import pytest
@@ -99,6 +100,33 @@ def test_c4_layer_three_steps_with_broadcast_vs_oracle():
     for i, (g, w) in enumerate(zip(got, want)):
         rel = np.linalg.norm(g.astype(np.float64) - w) / np.linalg.norm(w)
         mx = np.abs(g - w).max() / np.abs(w).max()
+        assert rel < REL_TOL_CFG and mx < MAX_TOL_CFG, (i, rel, mx)
+
+
+def test_c5_layer_two_steps_with_broadcast_vs_oracle():
+    """C5 (Open-Sora 720p 4s) at full shape for one layer: D1152, H16, T32 (the attn_tm
+    T = 32 path), S3600 (45 x 80), M300, cross in the temporal block, CFG batch 2; step 1
+    broadcasts every site computed at step 0.  The oracle evaluates the 3600-token
+    spatial attention in chunks (53 GB of logits unchunked)."""
+    cfg = ModelConfig(layers=1, hidden=1152, heads=16, frames=32, spatial_tokens=3600, text_tokens=300,
+                      cross_in_temporal=True)
+    params = init_model(cfg, seed=11)
+    src = np.zeros((2, 1, 4), dtype=np.int32)  # step 1 reuses step 0 everywhere
+    table = DecisionTable(src)
+    ids = np.arange(300) % 256
+    den = Denoiser(params, make_schedule(2), table, ids, guidance=True, guidance_scale=4.0)
+    z = torch.from_numpy(initial_latent(params, 11, 2)).cuda()
+    got = []
+    den.run(z, on_step=lambda i, zz: got.append(zz.cpu().numpy().copy()))
+    assert den.ctx.launches.sites_reused == 6
+    ocfg = orc.Cfg(1, 1152, 16, 32, 3600, 300, cross_in_temporal=True)
+    want = []
+    orc.sample(ocfg, orc.init_weights(ocfg, 11), orc.linear_timesteps(2), src, seed=11, text_ids=ids,
+               guidance=True, per_step=want)
+    for i, (g, w) in enumerate(zip(got, want)):
+        rel = np.linalg.norm(g.astype(np.float64) - w) / np.linalg.norm(w)
+        mx = np.abs(g - w).max() / np.abs(w).max()
+        print(f"C5 slice step {i}: relL2 {rel:.2e}, max {mx:.2e}")
         assert rel < REL_TOL_CFG and mx < MAX_TOL_CFG, (i, rel, mx)
 
 
