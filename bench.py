@@ -50,7 +50,11 @@ CONFIGS = {
     "C1cfg": dict(layers=4, hidden=144, heads=2, frames=8, spatial_tokens=1024, text_tokens=16, cross=True,
                   steps=10, preset="opensora-pab246", batch=2),
 }
-METRIC = "s/video denoising latency (PAB, opensora-pab246)"
+METRIC = "s/video denoising latency (PAB, opensora-pab246)"  # the C3 headline; other configs name their preset
+
+
+def metric_for(c):
+    return f"s/video denoising latency (PAB, {c['preset']})"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -252,7 +256,7 @@ def run_reference(args, c):
     v = statistics.median(r["value"] for r in runs)
     base = dict(runs[0], value=v, samples_s=[r["measured_sample_s"] for r in runs])
     line = {
-        "metric": METRIC, "value": v, "unit": "s/video", "n_gpus": args.gpus, "steps": args.steps,
+        "metric": metric_for(c), "value": v, "unit": "s/video", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": min(args.warmup, 1), "ms_per_step": v * 1000.0, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded splitmix64 weights and x_T)",
         "config": {"workload": args.config, **{k: c[k] for k in ("layers", "hidden", "heads", "frames",
@@ -580,7 +584,7 @@ def main():
         # the CPU reference beside the GPU number: rank 0 at N=1 only (the scaling runs skip it)
         base = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(c)
         line = {
-            "metric": METRIC, "value": ms / 1000.0, "unit": "s/video", "n_gpus": world, "steps": args.steps,
+            "metric": metric_for(c), "value": ms / 1000.0, "unit": "s/video", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded splitmix64 weights and x_T)",
             "config": {"workload": args.config, "layers": cfg.layers, "hidden": cfg.hidden, "heads": cfg.heads,
