@@ -225,7 +225,7 @@ def test_peer_barrier_timeout_reports_instead_of_hanging():
         px.check()
 
 
-def _nccl_worker(rank, world, port, q):
+def _nccl_worker(rank, world, port, q, transport="nccl"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
@@ -242,10 +242,12 @@ def _nccl_worker(rank, world, port, q):
         sched = make_schedule(8)
         pol = PabPolicy(2, 3, 2, window=(990.0, 10.0))
         table = build_schedule(pol, sched, cfg.layers)
-        par = run_parallel(params, sched, pol, world, "broadcast_sp", seed=7, guidance=True, table=table)
-        # the same run replayed as one CUDA graph with the NCCL all-to-alls captured inside
+        par = run_parallel(params, sched, pol, world, "broadcast_sp", seed=7, guidance=True, table=table,
+                           transport=transport)
+        # the same run replayed as one CUDA graph with the exchanges (NCCL all-to-alls or peer
+        # stores / loads + device barriers) captured inside
         den = ShardedDenoiser(params, sched, table, np.arange(12), guidance=True, guidance_scale=4.0, rank=rank,
-                              world=world)
+                              world=world, transport=transport)
         x = torch.from_numpy(initial_latent(params, 7, 2)).cuda()
         z = den.shard_input(x)
         den.capture_graph()
@@ -270,10 +272,12 @@ def _nccl_worker(rank, world, port, q):
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="NCCL broadcast SP needs >= 2 GPUs (the gpurun box has one)")
-def test_nccl_broadcast_sp_vs_oracle_and_graph():
-    """Broadcast SP over NCCL on real GPUs (one process per GPU): latents vs the CPU oracle's
-    serial run within the CFG gate, and a CUDA-graph replay with the all-to-alls captured
-    equal to the eager run bit for bit."""
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_nccl_broadcast_sp_vs_oracle_and_graph(transport):
+    """Broadcast SP on real GPUs (one process per GPU, NCCL group): the NCCL all-to-all and
+    the NVLink peer-memory transports, latents vs the CPU oracle's serial run within the CFG
+    gate, and a CUDA-graph replay with the exchanges captured equal to the eager run bit
+    for bit."""
     from gates import MAX_TOL_CFG, REL_TOL_CFG
 
     world = min(torch.cuda.device_count(), 8)
@@ -281,7 +285,7 @@ def test_nccl_broadcast_sp_vs_oracle_and_graph():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_nccl_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_nccl_worker, args=(r, world, port, q, transport)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in procs]
