@@ -427,9 +427,10 @@ class _SPTemporal:
         if source == st.step:
             store = d.should_store(li, TM)
             p = lp.temporal
+            gamma, beta = self._ln(p)
             kernels.residual_modnorm_sp(st.src.view(-1, ctx.D), st.r.view(-1, ctx.D), st.pending, ctx.h,
                                         (ctx.B, ctx.T, ctx.S, ctx.D), self.W, mod=st.mods[li, MOD_TEMPORAL],
-                                        mode=1)
+                                        gamma=gamma, beta=beta, mode=1)
             ctx.launches.prologue_calls += 1
             st.src, st.pending = st.r, []
             exchange_frames_to_tokens(self.h_send, self.h_tok, self.group)
@@ -460,6 +461,12 @@ class _SPTemporal:
         st.pending.append(o)
         st.record(li, TM, "t", decision, source, o)
 
+    def _ln(self, p):
+        """LayerNorm affine of a site (None, None at the reference init: gamma = 1, beta = 0)."""
+        if self.ctx.params.ln_identity:
+            return None, None
+        return p.ln_gamma, p.ln_beta
+
     def _compute_peer(self, st, li, lp, store):
         """Computed temporal site over NVLink peer memory: the prologue's stores are the
         frames->tokens exchange, the next prologue's loads the tokens->frames one."""
@@ -471,8 +478,9 @@ class _SPTemporal:
         ctx, p, px = self.ctx, lp.temporal, self.px
         if st.wants_output():
             raise ValidationError("output digests/snapshots are not available with the peer transport")
+        gamma, beta = self._ln(p)
         kernels.residual_modnorm(st.src.view(-1, ctx.D), st.r.view(-1, ctx.D), st.pending, mod=st.mods[li, MOD_TEMPORAL],
-                                 mode=1, shape=(ctx.B, ctx.T, ctx.S), h_peer=(px, "h_tok"))
+                                 gamma=gamma, beta=beta, mode=1, shape=(ctx.B, ctx.T, ctx.S), h_peer=(px, "h_tok"))
         ctx.launches.prologue_calls += 1
         st.src, st.pending = st.r, []
         px.barrier()  # every rank's h rows have landed in every h_tok
