@@ -463,7 +463,7 @@ extern "C" int pab_residual_modnorm_peer(const float* x_in, float* x_out, const 
                                          const float* mod, void* h_out, void* const* peer_h, int64_t n_b,
                                          int64_t n_t, int64_t n_s, int64_t n_w, int rank, int D, float eps,
                                          int mode, int h_layout, void* stream) {
-    if (n_b < 1 || n_t < 1 || n_s < 1 || n_w < 1 || n_w > PAB_MAX_PEERS) return PAB_ERR_SHAPE;
+    if (n_b < 1 || n_t < 1 || n_s < 1 || n_w < 1) return PAB_ERR_SHAPE;
     if (n_pending < 0 || n_pending > PAB_MAX_PENDING) return PAB_ERR_SHAPE;
     if (rank < 0 || rank >= n_w) return PAB_ERR_INVALID;
     TmState tm{0u, n_t, n_s};
@@ -481,7 +481,9 @@ extern "C" int pab_residual_modnorm_peer(const float* x_in, float* x_out, const 
         else if (l == PAB_LAYOUT_PEER) { tm.peer |= 1u << i; a2a = true; ++n_peer; }
         else if (l != PAB_LAYOUT_FRAME) return PAB_ERR_INVALID;
     }
-    // one peer-resident term per launch (the temporal output of the preceding site)
+    // one peer-resident term per launch (the temporal output of the preceding site); the peer
+    // forms address at most PAB_MAX_PEERS ranks (the all-to-all orders take any n_w)
+    if ((n_peer > 0 || h_layout == PAB_LAYOUT_PEER) && n_w > PAB_MAX_PEERS) return PAB_ERR_SHAPE;
     if (n_peer > 1 || (n_peer == 1 && peer_src == nullptr)) return PAB_ERR_INVALID;
     if (peer_copy != nullptr && n_peer != 1) return PAB_ERR_INVALID;
     if (n_peer == 1)
@@ -513,13 +515,6 @@ extern "C" int pab_residual_modnorm_ex(const float* x_in, float* x_out, const vo
     if (h_layout == PAB_LAYOUT_PEER) return PAB_ERR_INVALID;
     for (int i = 0; term_layout && i < n_pending; ++i)
         if (term_layout[i] == PAB_LAYOUT_PEER) return PAB_ERR_INVALID;
-    if (n_w > PAB_MAX_PEERS) {
-        // plain all-to-all orders work for any W; only the peer forms are bounded
-        bool any = h_layout == PAB_LAYOUT_A2A;
-        for (int i = 0; term_layout && i < n_pending; ++i) any = any || term_layout[i] == PAB_LAYOUT_A2A;
-        if (any) return PAB_ERR_SHAPE;
-        n_w = 1;
-    }
     return pab_residual_modnorm_peer(x_in, x_out, pending, term_layout, n_pending, nullptr, nullptr, gamma, beta,
                                      mod, h_out, nullptr, n_b, n_t, n_s, n_w, 0, D, eps, mode, h_layout, stream);
 }

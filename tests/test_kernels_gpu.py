@@ -254,7 +254,7 @@ def test_fill_uniform_matches_host_stream():
     assert torch.equal(dst16, torch.from_numpy(want).to(DEV).to(torch.bfloat16))
 
 
-@pytest.mark.parametrize("W,mode", [(2, 1), (4, 2), (8, 0)])
+@pytest.mark.parametrize("W,mode", [(2, 1), (4, 2), (8, 0), (16, 1)])
 def test_residual_modnorm_all_to_all_order_terms(W, mode):
     """PAB_LAYOUT_A2A pending terms (the sequence-parallel temporal site's received output,
     (W_src, T/W, B, S/W, D)) are added through the prologue's row map, equal to unpacking
@@ -279,3 +279,51 @@ def test_residual_modnorm_all_to_all_order_terms(W, mode):
         check_close(h, ln * (1.0 + mod[D:]) + mod[:D], "modnorm a2a", 6e-3)
     elif mode == 2:
         assert torch.equal(h, want.to(torch.bfloat16))
+
+
+class _FakePeers:
+    """The W ranks' token buffers of a PeerExchange, all in this process (kernel test)."""
+
+    def __init__(self, rank, bufs):
+        from paper_2408_12588_b200 import _lib
+
+        self.rank, self.world, self.bufs = rank, len(next(iter(bufs.values()))), bufs
+        self._arr = {k: _lib.ptr_array([t.data_ptr() for t in v]) for k, v in bufs.items()}
+
+    def ptrs(self, name):
+        return self._arr[name]
+
+
+@pytest.mark.parametrize("W,me", [(2, 1), (4, 2), (8, 7)])
+def test_residual_modnorm_peer_layouts(W, me):
+    """PAB_LAYOUT_PEER: the pending temporal output read straight out of the W ranks' token
+    buffers (plus its frame-major cache copy), and h stored straight into the ranks' h
+    token buffers -- equal to the all-to-all order forms (which equal reshard)."""
+    B, Tl, S, D = 2, 3, 64, 144
+    Sw, T, rows = S // W, Tl * W, B * Tl * S
+    g = torch.Generator(device=DEV).manual_seed(W + me)
+    x = torch.randn(rows, D, device=DEV, generator=g)
+    o_tok = [torch.randn(T, B, Sw, D, device=DEV, generator=g).to(torch.bfloat16) for _ in range(W)]
+    h_tok = [torch.full((T, B, Sw, D), 9.0, device=DEV, dtype=torch.bfloat16) for _ in range(W)]
+    mod = torch.randn(2 * D, device=DEV, generator=g) * 0.1
+    px = _FakePeers(me, {"o_tok": o_tok, "h_tok": h_tok})
+    term = o_tok[me].view(o_tok[me].shape)
+    term.pab_peer = (px, "o_tok")
+    copy = torch.empty(B, Tl, S, D, device=DEV, dtype=torch.bfloat16)
+    term.pab_peer_copy = copy
+    x_out = torch.empty_like(x)
+    kernels.residual_modnorm(x, x_out, [term], mod=mod, mode=1, shape=(B, Tl, S), h_peer=(px, "h_tok"))
+    # what rank `me` receives in an all-to-all: rank src's token rows of frames [me*Tl, (me+1)*Tl)
+    recv = torch.stack([o_tok[src][me * Tl:(me + 1) * Tl] for src in range(W)])  # (W_src, Tl, B, Sw, D)
+    frame = recv.permute(2, 1, 0, 3, 4).reshape(B, Tl, S, D)
+    assert torch.equal(copy, frame)
+    want = x + frame.reshape(rows, D).float()
+    assert torch.equal(x_out, want)
+    ln = torch.nn.functional.layer_norm(want, (D,), eps=1e-5) * (1.0 + mod[D:]) + mod[:D]
+    h_frame = ln.view(B, Tl, W, Sw, D)
+    for dst in range(W):
+        got = h_tok[dst][me * Tl:(me + 1) * Tl]  # (Tl, B, Sw, D) rows this rank stored
+        check_close(got.reshape(-1, D), h_frame[:, :, dst].permute(1, 0, 2, 3).reshape(-1, D),
+                    "peer h store", 6e-3)
+        others = torch.cat([h_tok[dst][:me * Tl], h_tok[dst][(me + 1) * Tl:]])
+        assert bool((others == 9.0).all())
