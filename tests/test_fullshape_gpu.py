@@ -1,7 +1,8 @@
 """Full-size parity slices: one layer of the C2/C3/C4 blocks at
 their real shapes (D1152, H16, T16, S1024/1560, M120/300, CFG batch 2) for a few
 denoising steps whose tables broadcast sites, against the CPU oracle; a 4-layer
-x 30-step C3 run against an oracle fixture (tests/golden/c3_deep.npz); a C5 layer
+x 30-step C3 run and a 4-layer x 50-step C2 run against oracle fixtures
+(tests/golden/c3_deep.npz, c2_deep.npz); a C5 layer
 (T32, S3600) for two steps; and C5's 3600-token spatial attention at op level against
 a torch fp32 reference."""
 
@@ -101,6 +102,98 @@ def test_c4_layer_three_steps_with_broadcast_vs_oracle():
         rel = np.linalg.norm(g.astype(np.float64) - w) / np.linalg.norm(w)
         mx = np.abs(g - w).max() / np.abs(w).max()
         assert rel < REL_TOL_CFG and mx < MAX_TOL_CFG, (i, rel, mx)
+
+
+def test_c5_layer_two_steps_with_broadcast_vs_oracle():
+    """C5 (Open-Sora 720p 4s) at full shape for one layer: D1152, H16, T32 (the attn_tm
+    T = 32 path), S3600 (45 x 80), M300, cross in the temporal block, CFG batch 2; step 1
+    broadcasts every site computed at step 0.  The oracle evaluates the 3600-token
+    spatial attention in chunks (53 GB of logits unchunked)."""
+    cfg = ModelConfig(layers=1, hidden=1152, heads=16, frames=32, spatial_tokens=3600, text_tokens=300,
+                      cross_in_temporal=True)
+    params = init_model(cfg, seed=11)
+    src = np.zeros((2, 1, 4), dtype=np.int32)  # step 1 reuses step 0 everywhere
+    table = DecisionTable(src)
+    ids = np.arange(300) % 256
+    den = Denoiser(params, make_schedule(2), table, ids, guidance=True, guidance_scale=4.0)
+    z = torch.from_numpy(initial_latent(params, 11, 2)).cuda()
+    got = []
+    den.run(z, on_step=lambda i, zz: got.append(zz.cpu().numpy().copy()))
+    assert den.ctx.launches.sites_reused == 6
+    ocfg = orc.Cfg(1, 1152, 16, 32, 3600, 300, cross_in_temporal=True)
+    want = []
+    orc.sample(ocfg, orc.init_weights(ocfg, 11), orc.linear_timesteps(2), src, seed=11, text_ids=ids,
+               guidance=True, per_step=want)
+    for i, (g, w) in enumerate(zip(got, want)):
+        rel = np.linalg.norm(g.astype(np.float64) - w) / np.linalg.norm(w)
+        mx = np.abs(g - w).max() / np.abs(w).max()
+        print(f"C5 slice step {i}: relL2 {rel:.2e}, max {mx:.2e}")
+        assert rel < REL_TOL_CFG and mx < MAX_TOL_CFG, (i, rel, mx)
+
+
+def test_c5_spatial_attention_3600_tokens():
+    B, S, H, dh = 2, 3600, 16, 72
+    D = H * dh
+    g = torch.Generator(device="cuda").manual_seed(3)
+    qkv = torch.randn(B * S, 3 * D, device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.empty(B * S, D, device="cuda", dtype=torch.bfloat16)
+    ld = 3 * D
+    a = kernels.attn_args(qkv[:, :D], qkv[:, D:2 * D], qkv[:, 2 * D:], out, (S * ld, 0, ld), (S * ld, 0, ld),
+                          (S * ld, 0, ld), (S * D, 0, D), B, 1, S, S, H, dh)
+    assert kernels.attention_select(a) == kernels.IMPL_TCGEN05
+    kernels.attention(a)
+    x = qkv.float().view(B, S, 3, H, dh).permute(2, 0, 3, 1, 4)
+    ref = torch.softmax(x[0] @ x[1].transpose(-1, -2) / dh**0.5, -1) @ x[2]
+    ref = ref.permute(0, 2, 1, 3).reshape(B * S, D)
+    rel = float((out.float() - ref).norm() / ref.norm())
+    assert rel < 1.2e-2, rel
+
+
+# fixtures of tests/golden/make_deep.py (make_c3_deep.py wrote c3 before the config field existed)
+_DEEP_DEFAULT = {"c3": (4, 1152, 16, 16, 1560, 300, 1, 30)}
+
+
+@pytest.mark.parametrize("name", ["c3", "c2"])
+def test_deep_multilayer_full_schedule_vs_oracle_fixture(name):
+    """A config at full width with 4 of its 28 layers over its whole PAB schedule (CFG g=4)
+    against the CPU oracle's run stored in tests/golden/<name>_deep.npz
+    (tests/golden/make_deep.py): per-step latent norm, max|x| and a strided 8192-element
+    subsample.  C3: opensora-pab246, 30 steps, cross attention in the temporal block;
+    C2: latte-pab235, 50 steps, M = 120.  Broadcast reuse compounds over the schedule
+    here, which the one-layer slices cannot show."""
+    import os
+
+    path = os.path.join(os.path.dirname(__file__), "golden", f"{name}_deep.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"tests/golden/{name}_deep.npz not generated (tests/golden/make_deep.py {name})")
+    fx = np.load(path)
+    L, D, H, T, S, M, cit, N = (int(v) for v in (fx["config"] if "config" in fx else _DEEP_DEFAULT[name]))
+    cfg = ModelConfig(layers=L, hidden=D, heads=H, frames=T, spatial_tokens=S, text_tokens=M,
+                      cross_in_temporal=bool(cit))
+    params = init_model(cfg, seed=11)
+    table = DecisionTable(fx["table"])
+    den = Denoiser(params, make_schedule(N), table, np.arange(M) % 256, guidance=True, guidance_scale=4.0)
+    z = torch.from_numpy(initial_latent(params, 11, 2)).cuda()
+    idx = torch.from_numpy(fx["idx"]).cuda()
+    got_sub, got_norm, got_max = [], [], []
+
+    def on_step(i, zz):
+        flat = zz.reshape(-1)
+        got_sub.append(flat[idx].cpu().numpy().astype(np.float64))
+        got_norm.append(float(flat.double().norm()))
+        got_max.append(float(flat.abs().max()))
+
+    den.run(z, on_step=on_step)
+    assert den.ctx.launches.sites_reused > 0
+    worst = (0.0, 0.0, 0.0)
+    for i in range(N):
+        w = fx["sub"][i].astype(np.float64)
+        rel = np.linalg.norm(got_sub[i] - w) / np.linalg.norm(w)
+        mx = np.abs(got_sub[i] - w).max() / float(fx["maxabs"][i])
+        rn = abs(got_norm[i] - float(fx["norms"][i])) / float(fx["norms"][i])
+        worst = tuple(max(a, b) for a, b in zip(worst, (rel, mx, rn)))
+        assert rel < REL_TOL_CFG and mx < MAX_TOL_CFG and rn < REL_TOL_CFG, (i, rel, mx, rn)
+    print(f"{name} L{L} x {N} steps vs oracle: worst relL2 {worst[0]:.2e}, max {worst[1]:.2e}, norm {worst[2]:.2e}")
 
 
 def test_c5_layer_two_steps_with_broadcast_vs_oracle():
