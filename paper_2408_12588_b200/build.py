@@ -34,7 +34,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OBJ_DIR, exist_ok=True)
     headers = [os.path.join(CSRC, h) for h in HEADERS]
     hdr_time = _newest(headers)
-    objs = []
+    objs, cmds = [], []
     for src in SOURCES:
         sp = os.path.join(CSRC, src)
         op = os.path.join(OBJ_DIR, src.replace(".cu", ".o"))
@@ -44,7 +44,13 @@ def build(verbose: bool = False, force: bool = False) -> str:
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
                 print(" ".join(cmd), flush=True)
-            subprocess.run(cmd, check=True)
+            cmds.append(cmd)
+    # translation units compile independently: run them side by side
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        for f in [ex.submit(subprocess.run, c, check=True) for c in cmds]:
+            f.result()
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < _newest(objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
         if verbose:
