@@ -75,10 +75,12 @@ def model_config(c):
                        cross_in_temporal=c["cross"])
 
 
-def video_flops(cfg, table, batch):
+def video_flops(cfg, table, batch, cross_live=None):
     """Algorithmic flops of one video under a decision table (2 flop/MAC, all
     GEMMs + attention contractions of computed sites; reference profiler
-    flop model, profiler.py:176-226, without elementwise constants)."""
+    flop model, profiler.py:176-226, without elementwise constants).
+    cross_live: batch rows whose cross sites actually run (the engine skips the
+    all-null-text CFG row, whose output is exactly 0); None = the reference model."""
     import numpy as np
 
     D, R, T, S, M, H = cfg.hidden, cfg.mlp_hidden, cfg.frames, cfg.spatial_tokens, cfg.text_tokens, cfg.heads
@@ -86,7 +88,8 @@ def video_flops(cfg, table, batch):
     site = {
         "spatial": 2 * rows * D * 3 * D + 4 * batch * T * S * S * D + 2 * rows * D * D,
         "temporal": 2 * rows * D * 3 * D + 4 * batch * S * T * T * D + 2 * rows * D * D,
-        "cross": 2 * rows * D * D + 4 * rows * M * D + 2 * rows * D * D,
+        "cross": (2 * rows * D * D + 4 * rows * M * D + 2 * rows * D * D)
+                 * (1 if cross_live is None else cross_live) // (1 if cross_live is None else batch),
         "mlp": 2 * 2 * rows * D * R,
     }
     mult = {"spatial": 1, "temporal": 1, "cross": 1 + int(cfg.cross_in_temporal), "mlp": 2}
@@ -579,6 +582,7 @@ def main():
                 "spatial_attention_frac": kern_step["spatial_attn"]["frac_bf16_peak"],
                 "spatial_attention_frac_burst": kern["spatial_attn"]["frac_bf16_peak"]}
     flops_pab, _ = video_flops(cfg, table, c["batch"])
+    flops_exec, _ = video_flops(cfg, table, c["batch"], cross_live=1 if guidance else c["batch"])
 
     if rank == 0:
         # the CPU reference beside the GPU number: rank 0 at N=1 only (the scaling runs skip it)
@@ -599,8 +603,11 @@ def main():
                        "none_s_per_video": None if none_ms is None else none_ms / 1000.0,
                        "pab_speedup_vs_none": None if none_ms is None else none_ms / ms,
                        "video_tflop_pab": flops_pab / 1e12, "achieved_tflops_video": flops_pab / (ms / 1e3) / 1e12,
-                       "flop_note": "reference FLOP model (includes the null-text CFG half of the cross "
-                                    "sites, which this engine skips because its output is exactly 0)"},
+                       "video_tflop_executed": flops_exec / 1e12,
+                       "achieved_tflops_video_executed": flops_exec / (ms / 1e3) / 1e12,
+                       "flop_note": "video_tflop_pab: reference FLOP model (includes the null-text CFG half of "
+                                    "the cross sites); *_executed: without that half, which this engine skips "
+                                    "because its output is exactly 0"},
             "e2e": {"value": e2e_ms / 1000.0, "unit": "s/video", "h2d_bytes_per_step": io_bytes,
                     "d2h_bytes_per_step": io_bytes},
             "gpu_launches": launches,
