@@ -65,7 +65,10 @@ constexpr int kSoftmaxWarps = 8 * kSplit;
 constexpr bool kEpiWarps = PAB_FA_EPI_WARPS != 0 && kSplit == 1;
 constexpr int kEpiWarp0 = 12;
 constexpr int kThreads = kEpiWarps ? 512 : 32 * (kSoftmaxWarps + 3);
-constexpr int kRegSoftmax = 176, kRegAux = 80;
+#ifndef PAB_FA_REG_SOFTMAX
+#define PAB_FA_REG_SOFTMAX 176
+#endif
+constexpr int kRegSoftmax = PAB_FA_REG_SOFTMAX, kRegAux = (65536 / 256 - PAB_FA_REG_SOFTMAX) / 8 * 8;
 static_assert(!kEpiWarps || 256 * kRegSoftmax + 256 * kRegAux <= 65536, "register file");
 constexpr int kRows = 128;   // query rows per tile == TMEM lanes
 constexpr int kKv = 112;     // keys per KV tile
