@@ -153,14 +153,15 @@ def test_c5_spatial_attention_3600_tokens():
 _DEEP_DEFAULT = {"c3": (4, 1152, 16, 16, 1560, 300, 1, 30)}
 
 
-@pytest.mark.parametrize("name", ["c3", "c2"])
+@pytest.mark.parametrize("name", ["c3", "c2", "c4"])
 def test_deep_multilayer_full_schedule_vs_oracle_fixture(name):
     """A config at full width with 4 of its 28 layers over its whole PAB schedule (CFG g=4)
     against the CPU oracle's run stored in tests/golden/<name>_deep.npz
     (tests/golden/make_deep.py): per-step latent norm, max|x| and a strided 8192-element
     subsample.  C3: opensora-pab246, 30 steps, cross attention in the temporal block;
-    C2: latte-pab235, 50 steps, M = 120.  Broadcast reuse compounds over the schedule
-    here, which the one-layer slices cannot show."""
+    C2: latte-pab235, 50 steps, M = 120; C4: opensoraplan-pab246, 150 steps (2 layers).
+    Broadcast reuse compounds over the schedule here, which the one-layer slices cannot
+    show."""
     import os
 
     path = os.path.join(os.path.dirname(__file__), "golden", f"{name}_deep.npz")
