@@ -102,8 +102,25 @@ static_assert(!kEpiWarps || kPvSplit, "the dedicated epilogue needs per-tile o_d
 #define PAB_FA_POLY_DIV 3   // one column pair in PAB_FA_POLY_DIV on the FMA pipe (0: MUFU only)
 #endif
 
+// Division by a kernel-invariant divisor as multiply-high + shift (valid for 0 <= n < 2^31):
+// the item decode runs on the softmax and MMA warps' critical path at every item boundary,
+// where hardware-less integer division (MUFU.RCP + fix-up chains) cost ~300 clk per item.
+struct FastDiv {
+    uint32_t d, m, s;
+};
+static inline FastDiv make_fastdiv(uint32_t d) {
+    if (d == 0) d = 1;  // empty problems: never used
+    uint32_t s = 0;
+    while ((1ull << s) < d) ++s;
+    return FastDiv{d, (uint32_t)(((1ull << 32) * ((1ull << s) - d)) / d + 1), s};
+}
+__device__ __forceinline__ int fdiv(int n, const FastDiv& f) {
+    return (int)((__umulhi((uint32_t)n, f.m) + (uint32_t)n) >> f.s);
+}
+
 struct Params {
     int n_q, n_k, n_b, heads, dh;
+    FastDiv f_heads, f_full, f_b;  // heads, pairs with two tiles (n_full), n_b
     int row_tiles;     // 128-row query tiles per (problem, head)
     int n_kv;          // KV tiles per problem
     int n_pairs;       // query-tile pairs per (problem, head)
@@ -367,16 +384,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         int pair, az;
         if (item >= items_full) {  // single-tile items (pair n_full) of every (problem, head)
             const int rest = item - items_full;
-            it.h = rest % p.heads;
-            az = rest / p.heads;
+            az = fdiv(rest, p.f_heads);
+            it.h = rest - az * p.heads;
             pair = n_full;
         } else {
-            it.h = item % p.heads;
-            const int rest = item / p.heads;
-            pair = rest % n_full;
-            az = rest / n_full;
+            const int rest = fdiv(item, p.f_heads);
+            it.h = item - rest * p.heads;
+            az = fdiv(rest, p.f_full);
+            pair = rest - az * n_full;
         }
-        it.a_idx = az / p.n_b;
+        it.a_idx = fdiv(az, p.f_b);
         it.b_idx = az - it.a_idx * p.n_b;
         it.tile0 = 2 * pair;
         it.two = it.tile0 + 1 < p.row_tiles;
@@ -537,9 +554,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         bool have_prev = false;
         int it_n = 0;  // iterations of this tile (tile 1 skips single-tile items)
         for (int c = 0; c < my_items; ++c) {
+            FA_TRACE(trc, it_n, t, 6);
             const Item it = decode((int)blockIdx.x + c * (int)gridDim.x);
             const bool active = (t == 0) || it.two;
             float m_run = -INFINITY;
+            FA_TRACE(trc, it_n, t, 7);
             for (int j = 0; j < n_kv; ++j, ++it_n) {
                 FA_TRACE(trc, it_n, t, 0);
                 mbar_wait(&bars->s_full, it_n & 1);
@@ -1057,6 +1076,9 @@ int launch(const pab_attn_args* a, cudaStream_t st) {
     const int64_t items = (int64_t)p.n_pairs * a->heads * a->n_a * a->n_b;
     if (items > 0x7fffffff) return PAB_ERR_UNSUPPORTED;
     p.n_items = (int)items;
+    p.f_heads = make_fastdiv((uint32_t)a->heads);
+    p.f_full = make_fastdiv((uint32_t)(PAB_FA_SINGLES_LAST ? p.row_tiles / 2 : p.n_pairs));
+    p.f_b = make_fastdiv((uint32_t)a->n_b);
     static int num_sms = 0;
     if (num_sms == 0) {
         int dev = 0;

@@ -31,7 +31,7 @@ torch.cuda.synchronize()
 lib.pab_attn_debug_trace(None)
 tr = buf.view(64, 2, 16).cpu()
 t0 = int(tr[tr > 0].min())
-names = {0: "sm:wait_S", 1: "sm:S_ready", 2: "sm:S_loaded", 3: "sm:max_done", 4: "sm:exp_done", 5: "sm:p_full"}
+names = {6: "sm:item_top", 7: "sm:decoded", 0: "sm:wait_S", 1: "sm:S_ready", 2: "sm:S_loaded", 3: "sm:max_done", 4: "sm:exp_done", 5: "sm:p_full"}
 # MMA events are logged under tile 0 (S issue) / tile 1 (PV issue)
 mma_names = {(0, 10): "mma:wait_sfree", (0, 8): "mma:S_go", (1, 10): "mma:wait_P", (1, 8): "mma:PV_go",
              (1, 9): "mma:PV_issued"}
