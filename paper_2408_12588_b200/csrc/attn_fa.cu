@@ -553,10 +553,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         Item prev;
         bool have_prev = false;
         int it_n = 0;  // iterations of this tile (tile 1 skips single-tile items)
+        // the softmax warps only need each item's `two` flag: decoded 32 items at a time (one
+        // item per lane, ballot), so an item boundary costs them a bit test instead of a decode
+        uint32_t two_bits = 0;
         for (int c = 0; c < my_items; ++c) {
             FA_TRACE(trc, it_n, t, 6);
-            const Item it = decode((int)blockIdx.x + c * (int)gridDim.x);
-            const bool active = (t == 0) || it.two;
+            if ((c & 31) == 0) {
+                const int ci = c + lane;
+                const bool tw = ci < my_items && decode((int)blockIdx.x + ci * (int)gridDim.x).two;
+                two_bits = __ballot_sync(0xffffffffu, tw);
+            }
+            Item it{};
+            if (!kEpiWarps) it = decode((int)blockIdx.x + c * (int)gridDim.x);  // for epilogue(prev)
+            const bool active = (t == 0) || ((two_bits >> (c & 31)) & 1u);
             float m_run = -INFINITY;
             FA_TRACE(trc, it_n, t, 7);
             for (int j = 0; j < n_kv; ++j, ++it_n) {
