@@ -743,7 +743,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 const bool active = (t == 0) || it.two;
                 uint8_t* stg_tile = smem + G::kX0 + t * kRows * G::kStageRow;
+#ifdef PAB_FA_DIAG_NOEPI  // timing diagnostic only: O never leaves TMEM (barrier hand-off kept)
+                if (false) {
+#else
                 if (active) {
+#endif
                     // the previous store of this staging tile has read its rows (the other tile's
                     // store, if it is the most recent one, may stay in flight)
                     if (issuer) {
@@ -779,7 +783,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->o_free[t]);
+#ifdef PAB_FA_DIAG_NOEPI
+                if (false) {
+#else
                 if (active) {
+#endif
                     fence_async_smem();  // generic-proxy smem writes -> visible to the TMA (async proxy)
                     asm volatile("bar.sync 11, 128;" ::: "memory");
 #ifndef PAB_FA_DIAG_EPI_NOSTORE
